@@ -1,0 +1,213 @@
+/*
+ * ba_attn.h — C ABI of libbaatt.so, the B200 (sm_100a) hot path of
+ * Block Approximate Sparse Attention (BA-Att, arXiv 2605.19726).
+ *
+ * The ABI follows the paper's statement of the problem, Algorithm 1
+ * (PAPER.md P:527-569): REQUIRE Q, K, V; block size B; per-query-block budget
+ * kappa; compensation weight beta  ->  RETURN sparse attention
+ * outputs in the original token order.
+ *
+ *   ba_select       Alg. 1 steps 1-10: norm ranking of Q and K
+ *                   (s = ||x||_2), permuted copies Q', K', V'
+ *                   (P:537), block means / per-dimension variances
+ *                   (P:282), block logits
+ *                   l = Qbar.Kbar/sqrt(d) (Eq. block-logit), the
+ *                   diagonal-variance compensation Delta (Eq.
+ *                   diag-variance-form), l' = l + beta*Delta
+ *                   (P:553-556), m' = softmax_row(l') and the
+ *                   top-kappa block mask M.
+ *   ba_sparse_attn  Alg. 1 steps 11-12: non-causal block-sparse
+ *                   attention of Q' over the K'/V' blocks with M = 1,
+ *                   online softmax renormalised over the selected support
+ *                   (P:263-264), rows written back to the original
+ *                   order via pi_q^{-1}.
+ *   ba_attention    both, end to end.
+ *
+ * Conventions (all calls):
+ *  - Device pointers unless a name says _host.  The library never allocates
+ *    or frees memory: the caller owns every buffer and the stream, and the
+ *    buffers must stay alive until the stream work completes.  Scratch comes
+ *    from a caller-provided workspace (sizes from the *_workspace_size calls).
+ *  - All calls are stream-ordered and asynchronous: they enqueue kernels on
+ *    `stream` and return without synchronising.  A launch failure is reported
+ *    as BA_ERR_CUDA (cudaGetLastError); an asynchronous fault surfaces at the
+ *    caller's next synchronisation.
+ *  - Validation is synchronous and happens before any launch; on error
+ *    nothing is enqueued and ba_last_error() names the offending field.
+ *  - No C++ exception crosses the ABI.  The library is thread-safe for
+ *    concurrent calls on different streams (no global mutable state other
+ *    than idempotent per-device kernel attributes and the thread-local error
+ *    string).
+ *  - Tensor layout: element (b, h, t, c) of q/k/v/out lives at
+ *    base + b*stride[0] + h*stride[1] + t*stride[2] + c (element units; the
+ *    feature stride is 1).  Strides and base pointers must be 16-byte aligned
+ *    (TMA).  d = head_dim is also the value dimension.
+ *  - Attention is non-causal (bidirectional) only (diffusion LMs and
+ *    DiTs).
+ *  - Numerics: bf16 inputs run on tcgen05 tensor cores with fp32
+ *    accumulation and fp32 online softmax; fp32 inputs run an fp32 SIMT
+ *    path.  Selection (stats, scores, softmax, top-kappa) is computed in fp64
+ *    so that masks match the fp64 oracle except at exact-threshold near-ties.
+ */
+#ifndef BA_ATTN_H_
+#define BA_ATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BA_ABI_VERSION 1
+
+typedef enum {
+  BA_OK = 0,
+  BA_ERR_INVALID_ARGUMENT = 1,   /* NULL pointer, non-positive size, bad enum, density not in (0,1] */
+  BA_ERR_SHAPE_MISMATCH = 2,     /* heads_q % heads_kv != 0, misaligned stride / pointer */
+  BA_ERR_UNSUPPORTED = 3,        /* valid but not implemented (head_dim, block_size, dtype combo) */
+  BA_ERR_WORKSPACE_TOO_SMALL = 4,
+  BA_ERR_CUDA = 5,               /* a CUDA runtime call or launch failed */
+  BA_ERR_EMPTY_MASK_ROW = 6      /* kappa < 1 (every mask row must be non-empty) */
+} ba_status;
+
+typedef enum { BA_DTYPE_BF16 = 0, BA_DTYPE_FP32 = 1 } ba_dtype;
+
+/* Which sides are norm-ranked (ablation Table). */
+typedef enum { BA_SORT_NONE = 0, BA_SORT_Q = 1, BA_SORT_K = 2, BA_SORT_QK = 3 } ba_sort_mode;
+
+/* Compensation of the block logits: none, or the diagonal-variance form
+ * Delta = (1/d) sum_t (VarQ_t Kbar_t^2 + VarK_t Qbar_t^2 + VarQ_t VarK_t)
+ * (Eq. diag-variance-form). */
+typedef enum { BA_COMP_NONE = 0, BA_COMP_DIAG = 1 } ba_comp_mode;
+
+/* Budget rule ("under different computational budgets"; Alg. 1 step 10
+ * P:560 top-kappa).  TOPP (cumulative mass >= top_p) is reserved. */
+typedef enum { BA_SELECT_TOPK = 0, BA_SELECT_TOPP = 1 } ba_select_mode;
+
+typedef struct {
+  int32_t batch;        /* b >= 1 */
+  int32_t heads_q;      /* H_q >= 1 */
+  int32_t heads_kv;     /* H_kv >= 1, heads_q % heads_kv == 0 (GQA: q-head h uses kv-head h / (H_q/H_kv)) */
+  int32_t head_dim;     /* d in {64, 128} */
+  int64_t len_q;        /* L_q >= 1; need not be a multiple of block_size (ragged last block) */
+  int64_t len_k;        /* L_k >= 1 */
+  int32_t block_size;   /* B in {64, 128}: N_q = ceil(L_q/B), N_k = ceil(L_k/B) */
+  int32_t dtype;        /* ba_dtype of q, k, v, out */
+  int64_t q_stride[3];  /* element strides for (batch, head, token); feature stride is 1 */
+  int64_t k_stride[3];
+  int64_t v_stride[3];
+  int64_t o_stride[3];
+} ba_problem;
+
+typedef struct {
+  int32_t sort;          /* ba_sort_mode; default BA_SORT_QK */
+  int64_t sort_window;   /* 0 = global sort; w > 0 sorts each run of w tokens independently ("(windowed) sort") */
+  int32_t comp;          /* ba_comp_mode; default BA_COMP_DIAG */
+  float beta;            /* compensation weight; default 1 */
+  int32_t select;        /* ba_select_mode; BA_SELECT_TOPK */
+  float density;         /* rho in (0, 1]; kappa = max(1, min(N_k, floor(rho*N_k + 1/2))) (reading A2) */
+  float top_p;           /* BA_SELECT_TOPP only (reserved) */
+  float softmax_scale;   /* 0 => 1/sqrt(head_dim) (Eq. sdpa) */
+} ba_params;
+
+/* Selection produced by ba_select and consumed by ba_sparse_attn.  Every
+ * buffer is caller-allocated device memory.  Required fields: perm_q,
+ * perm_k, q_sorted, k_sorted, v_sorted, kv_index, kv_count.  Optional
+ * (NULL = not written): everything else. */
+typedef struct {
+  int32_t *perm_q;       /* [b, H_q, L_q]   sorted position -> original token index (pi_q) */
+  int32_t *perm_k;       /* [b, H_kv, L_k]  pi_k */
+  void *q_sorted;        /* [b, H_q, L_q, d] contiguous, dtype: Q'_i = Q_{pi_q(i)} */
+  void *k_sorted;        /* [b, H_kv, L_k, d] contiguous: K'_j = K_{pi_k(j)} */
+  void *v_sorted;        /* [b, H_kv, L_k, d] contiguous: V'_j = V_{pi_k(j)} */
+  int32_t *kv_index;     /* [b, H_q, N_q, kappa] selected key blocks g_k, strictly ascending */
+  int32_t *kv_count;     /* [b, H_q, N_q] number of valid entries per row (== kappa for TOPK) */
+  uint8_t *mask;         /* [b, H_q, N_q, N_k] M in {0,1} */
+  double *block_prob;    /* [b, H_q, N_q, N_k] m' = softmax_row(l') */
+  double *logits;        /* [b, H_q, N_q, N_k] l' = l + beta*Delta */
+  double *threshold;     /* [b, H_q, N_q] tau = m' of the kappa-th selected block */
+  double *q_mean;        /* [b, H_q, N_q, d] Qbar over the sorted blocks */
+  double *q_var;         /* [b, H_q, N_q, d] population variance per dimension */
+  double *k_mean;        /* [b, H_kv, N_k, d] */
+  double *k_var;         /* [b, H_kv, N_k, d] */
+  float *q_key;          /* [b, H_q, L_q] sort key fp32(||q||^2) in ORIGINAL order (reading A4) */
+  float *k_key;          /* [b, H_kv, L_k] */
+} ba_selection;
+
+/* ABI version compiled into the library (== BA_ABI_VERSION of this header). */
+int ba_abi_version(void);
+
+/* N_q, N_k and kappa for a problem (no device work).  Returns
+ * BA_ERR_INVALID_ARGUMENT / BA_ERR_UNSUPPORTED on a bad problem. */
+ba_status ba_selection_sizes(const ba_problem *prob, const ba_params *params,
+                             int64_t *kappa, int64_t *n_q, int64_t *n_k);
+
+/* Scratch bytes needed by ba_select (sort buffers, histograms, stats and the
+ * fp64 score map when not supplied).  0 on an invalid problem. */
+size_t ba_select_workspace_size(const ba_problem *prob, const ba_params *params);
+
+/* Scratch bytes needed by ba_attention: ba_select's scratch plus every
+ * required ba_selection buffer (they are carved from the workspace). */
+size_t ba_attention_workspace_size(const ba_problem *prob, const ba_params *params);
+
+/* Alg. 1 steps 1-10.  q, k, v: device tensors in the ba_problem layout.
+ * Writes every non-NULL buffer of *sel.  workspace: >= ba_select_workspace_size
+ * bytes, 256-byte aligned. */
+ba_status ba_select(const ba_problem *prob, const ba_params *params,
+                    const void *q, const void *k, const void *v,
+                    const ba_selection *sel, void *workspace, size_t workspace_bytes,
+                    cudaStream_t stream);
+
+/* Alg. 1 steps 11-12.  Reads sel->q_sorted, k_sorted, v_sorted, kv_index,
+ * kv_count, perm_q (a caller may inject its own selection: kv_index rows must
+ * be ascending, unique, in [0, N_k), with kv_count >= 1).  out: original
+ * token order, ba_problem o_stride layout.  lse: optional [b, H_q, L_q] fp32
+ * natural-log log-sum-exp of the scaled logits per query row, original order. */
+ba_status ba_sparse_attn(const ba_problem *prob, const ba_params *params,
+                         const ba_selection *sel, void *out, float *lse,
+                         cudaStream_t stream);
+
+/* ba_select + ba_sparse_attn with the selection carved from the workspace
+ * (>= ba_attention_workspace_size bytes). */
+ba_status ba_attention(const ba_problem *prob, const ba_params *params,
+                       const void *q, const void *k, const void *v,
+                       void *out, float *lse, void *workspace, size_t workspace_bytes,
+                       cudaStream_t stream);
+
+/* Dense (all N_k blocks, no ranking) attention through the same tensor-core
+ * kernel: the 1/rho speed-of-light reference for the sparse path.  Same
+ * layouts as ba_attention; no workspace. */
+ba_status ba_dense_attn(const ba_problem *prob, const ba_params *params,
+                        const void *q, const void *k, const void *v,
+                        void *out, float *lse, cudaStream_t stream);
+
+/* End-to-end from HOST memory: copies q, k, v (host, contiguous [b,H,L,d];
+ * pinned for asynchronous copies) into device staging carved from the
+ * workspace, runs ba_attention, copies the output back to out_host
+ * (contiguous [b,H_q,L_q,d]).  Stream-ordered: synchronise `stream` before
+ * reading out_host.  Strides in *prob are ignored (contiguous assumed). */
+size_t ba_attention_host_workspace_size(const ba_problem *prob, const ba_params *params);
+ba_status ba_attention_host(const ba_problem *prob, const ba_params *params,
+                            const void *q_host, const void *k_host, const void *v_host,
+                            void *out_host, void *workspace, size_t workspace_bytes,
+                            cudaStream_t stream);
+
+/* Name of the attention kernel ba_sparse_attn / ba_attention / ba_dense_attn
+ * run for this problem: "attn_sm100_tcgen05" (bf16, d = 128, B = 128: tcgen05
+ * tensor cores, TMA, TMEM) or "attn_simt" (fp32 inputs, and bf16 shapes the
+ * tensor-core kernel does not cover yet).  "" on an invalid problem. */
+const char *ba_attention_kernel_name(const ba_problem *prob, const ba_params *params);
+
+/* Number of kernel launches the last successful call on this thread enqueued. */
+int ba_last_launch_count(void);
+
+const char *ba_status_string(ba_status status);
+/* Thread-local detail of the last error on this thread ("" if none). */
+const char *ba_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BA_ATTN_H_ */

@@ -1,0 +1,451 @@
+// api.cu — the C ABI of libbaatt.so (include/ba_attn.h): validation,
+// workspace carving and the launch sequence of Alg. 1.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/ba_attn.h"
+#include "kernels.h"
+
+using namespace baatt;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+ba_status fail(ba_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+ba_status cuda_check(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) return fail(BA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return BA_OK;
+}
+
+#define BA_TRY(expr)                    \
+  do {                                  \
+    ba_status _s = (expr);              \
+    if (_s != BA_OK) return _s;         \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Dims {
+  int64_t b, hq, hkv, lq, lk, d, B, nq, nk, kappa;
+  int dtype;
+  size_t esz;
+};
+
+ba_status check_problem(const ba_problem *p, const ba_params *pa, Dims *o) {
+  if (!p || !pa) return fail(BA_ERR_INVALID_ARGUMENT, "problem/params is NULL");
+  if (p->batch < 1) return fail(BA_ERR_INVALID_ARGUMENT, "batch = %d must be >= 1", p->batch);
+  if (p->heads_q < 1) return fail(BA_ERR_INVALID_ARGUMENT, "heads_q = %d must be >= 1", p->heads_q);
+  if (p->heads_kv < 1) return fail(BA_ERR_INVALID_ARGUMENT, "heads_kv = %d must be >= 1", p->heads_kv);
+  if (p->heads_q % p->heads_kv) return fail(BA_ERR_SHAPE_MISMATCH, "heads_q %% heads_kv = %d != 0", p->heads_q % p->heads_kv);
+  if (p->len_q < 1) return fail(BA_ERR_INVALID_ARGUMENT, "len_q = %lld must be >= 1", (long long)p->len_q);
+  if (p->len_k < 1) return fail(BA_ERR_INVALID_ARGUMENT, "len_k = %lld must be >= 1", (long long)p->len_k);
+  if (p->len_q > (1ll << 31) - 1 || p->len_k > (1ll << 31) - 1)
+    return fail(BA_ERR_UNSUPPORTED, "len_q/len_k must be < 2^31");
+  if (p->head_dim != 64 && p->head_dim != 128) return fail(BA_ERR_UNSUPPORTED, "head_dim = %d (supported: 64, 128)", p->head_dim);
+  if (p->block_size != 64 && p->block_size != 128) return fail(BA_ERR_UNSUPPORTED, "block_size = %d (supported: 64, 128)", p->block_size);
+  if (p->dtype != BA_DTYPE_BF16 && p->dtype != BA_DTYPE_FP32) return fail(BA_ERR_INVALID_ARGUMENT, "dtype = %d", p->dtype);
+  if (pa->sort < BA_SORT_NONE || pa->sort > BA_SORT_QK) return fail(BA_ERR_INVALID_ARGUMENT, "sort = %d", pa->sort);
+  if (pa->comp != BA_COMP_NONE && pa->comp != BA_COMP_DIAG) return fail(BA_ERR_INVALID_ARGUMENT, "comp = %d", pa->comp);
+  if (pa->select != BA_SELECT_TOPK) {
+    if (pa->select == BA_SELECT_TOPP) return fail(BA_ERR_UNSUPPORTED, "select = BA_SELECT_TOPP is reserved");
+    return fail(BA_ERR_INVALID_ARGUMENT, "select = %d", pa->select);
+  }
+  if (!(pa->density > 0.f && pa->density <= 1.f)) return fail(BA_ERR_INVALID_ARGUMENT, "density = %g not in (0, 1]", (double)pa->density);
+  if (!(pa->softmax_scale >= 0.f) || !isfinite(pa->softmax_scale)) return fail(BA_ERR_INVALID_ARGUMENT, "softmax_scale = %g", (double)pa->softmax_scale);
+  if (!isfinite(pa->beta)) return fail(BA_ERR_INVALID_ARGUMENT, "beta is not finite");
+  if (pa->sort_window < 0) return fail(BA_ERR_INVALID_ARGUMENT, "sort_window = %lld < 0", (long long)pa->sort_window);
+  o->b = p->batch; o->hq = p->heads_q; o->hkv = p->heads_kv; o->lq = p->len_q; o->lk = p->len_k;
+  o->d = p->head_dim; o->B = p->block_size; o->dtype = p->dtype;
+  o->esz = p->dtype == BA_DTYPE_BF16 ? 2 : 4;
+  o->nq = (o->lq + o->B - 1) / o->B;
+  o->nk = (o->lk + o->B - 1) / o->B;
+  // reading A2: kappa = max(1, min(N_k, floor(rho * N_k + 1/2))) in fp64
+  int64_t kap = (int64_t)floor((double)pa->density * (double)o->nk + 0.5);
+  if (kap > o->nk) kap = o->nk;
+  if (kap < 1) kap = 1;
+  o->kappa = kap;
+  return BA_OK;
+}
+
+ba_status check_strides(const char *name, const int64_t *s, size_t esz) {
+  for (int i = 0; i < 3; ++i) {
+    if (s[i] < 0) return fail(BA_ERR_SHAPE_MISMATCH, "%s_stride[%d] = %lld < 0", name, i, (long long)s[i]);
+    if ((s[i] * (int64_t)esz) % 16) return fail(BA_ERR_SHAPE_MISMATCH, "%s_stride[%d] = %lld is not 16-byte aligned", name, i, (long long)s[i]);
+  }
+  return BA_OK;
+}
+
+ba_status check_ptr(const char *name, const void *p) {
+  if (!p) return fail(BA_ERR_INVALID_ARGUMENT, "%s is NULL", name);
+  if (reinterpret_cast<uintptr_t>(p) % 16) return fail(BA_ERR_SHAPE_MISMATCH, "%s is not 16-byte aligned", name);
+  return BA_OK;
+}
+
+bool sort_q(const ba_params *pa) { return pa->sort == BA_SORT_Q || pa->sort == BA_SORT_QK; }
+bool sort_k(const ba_params *pa) { return pa->sort == BA_SORT_K || pa->sort == BA_SORT_QK; }
+
+SortGeom make_geom(const Dims &D, const ba_params *pa) {
+  SortGeom g;
+  int64_t base = 0, tile_base = 0, seg_base = 0;
+  const bool on[2] = {sort_q(pa), sort_k(pa)};
+  const int64_t heads[2] = {D.b * D.hq, D.b * D.hkv};
+  const int64_t L[2] = {D.lq, D.lk};
+  for (int s = 0; s < 2; ++s) {
+    if (!on[s]) continue;
+    SortSide sd;
+    sd.heads = heads[s];
+    sd.L = L[s];
+    sd.win = (pa->sort_window > 0 && pa->sort_window < L[s]) ? pa->sort_window : L[s];
+    sd.n_win = (sd.L + sd.win - 1) / sd.win;
+    sd.tiles_per_win = (sd.win + kSortTile - 1) / kSortTile;
+    sd.base = base;
+    sd.tile_base = tile_base;
+    sd.seg_base = seg_base;
+    base += sd.heads * sd.L;
+    tile_base += sd.tiles();
+    seg_base += sd.segs();
+    g.side[g.n_sides++] = sd;
+  }
+  g.keys_total = base;
+  g.tiles_total = tile_base;
+  g.segs_total = seg_base;
+  return g;
+}
+
+struct SelectPlan {
+  size_t keys_a, vals_a, keys_b, vals_b, hist, q_mean, q_var, k_mean, k_var, logits, total;
+};
+
+SelectPlan plan_select(const Dims &D, const ba_params *pa, const ba_selection *sel) {
+  SelectPlan p{};
+  SortGeom g = make_geom(D, pa);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
+  p.keys_a = take(4 * g.keys_total);
+  p.vals_a = take(4 * g.keys_total);
+  p.keys_b = take(4 * g.keys_total);
+  p.vals_b = take(4 * g.keys_total);
+  p.hist = take(4 * 256 * g.tiles_total);
+  const size_t qs = 8ull * D.b * D.hq * D.nq * D.d, ks = 8ull * D.b * D.hkv * D.nk * D.d;
+  p.q_mean = (sel && sel->q_mean) ? SIZE_MAX : take(qs);
+  p.q_var = (sel && sel->q_var) ? SIZE_MAX : take(qs);
+  p.k_mean = (sel && sel->k_mean) ? SIZE_MAX : take(ks);
+  p.k_var = (sel && sel->k_var) ? SIZE_MAX : take(ks);
+  p.logits = (sel && sel->logits) ? SIZE_MAX : take(8ull * D.b * D.hq * D.nq * D.nk);
+  p.total = off;
+  return p;
+}
+
+struct SelBufPlan {
+  size_t perm_q, perm_k, qs, ks, vs, kv_index, kv_count, total;
+};
+
+SelBufPlan plan_selbufs(const Dims &D) {
+  SelBufPlan p{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
+  p.perm_q = take(4ull * D.b * D.hq * D.lq);
+  p.perm_k = take(4ull * D.b * D.hkv * D.lk);
+  p.qs = take(D.esz * D.b * D.hq * D.lq * D.d);
+  p.ks = take(D.esz * D.b * D.hkv * D.lk * D.d);
+  p.vs = take(D.esz * D.b * D.hkv * D.lk * D.d);
+  p.kv_index = take(4ull * D.b * D.hq * D.nq * D.kappa);
+  p.kv_count = take(4ull * D.b * D.hq * D.nq);
+  p.total = off;
+  return p;
+}
+
+template <typename P>
+P *at(void *ws, size_t off) { return reinterpret_cast<P *>(static_cast<char *>(ws) + off); }
+
+ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa, const void *q,
+                     const void *k, const void *v, const ba_selection *sel, void *ws, size_t ws_bytes,
+                     cudaStream_t st) {
+  BA_TRY(check_ptr("q", q));
+  BA_TRY(check_ptr("k", k));
+  BA_TRY(check_ptr("v", v));
+  BA_TRY(check_strides("q", prob->q_stride, D.esz));
+  BA_TRY(check_strides("k", prob->k_stride, D.esz));
+  BA_TRY(check_strides("v", prob->v_stride, D.esz));
+  if (!sel) return fail(BA_ERR_INVALID_ARGUMENT, "selection is NULL");
+  if (!sel->perm_q || !sel->perm_k || !sel->kv_index || !sel->kv_count)
+    return fail(BA_ERR_INVALID_ARGUMENT, "selection perm_q/perm_k/kv_index/kv_count must be non-NULL");
+  BA_TRY(check_ptr("sel->q_sorted", sel->q_sorted));
+  BA_TRY(check_ptr("sel->k_sorted", sel->k_sorted));
+  BA_TRY(check_ptr("sel->v_sorted", sel->v_sorted));
+  const SelectPlan plan = plan_select(D, pa, sel);
+  if (ws_bytes < plan.total)
+    return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu < %zu", ws_bytes, plan.total);
+  if (plan.total && !ws) return fail(BA_ERR_INVALID_ARGUMENT, "workspace is NULL");
+  if (reinterpret_cast<uintptr_t>(ws) % kAlign) return fail(BA_ERR_SHAPE_MISMATCH, "workspace is not 256-byte aligned");
+
+  int launches = 0;
+  SortGeom g = make_geom(D, pa);
+  g.side[0].perm_out = nullptr;
+  uint32_t *keys_a = at<uint32_t>(ws, plan.keys_a), *vals_a = at<uint32_t>(ws, plan.vals_a);
+  uint32_t *keys_b = at<uint32_t>(ws, plan.keys_b), *vals_b = at<uint32_t>(ws, plan.vals_b);
+  // K1: norm keys (for every sorted side; also when the caller asked for them)
+  {
+    int si = 0;
+    if (sort_q(pa)) {
+      g.side[si].perm_out = sel->perm_q;
+      BA_TRY(cuda_check(launch_norm_keys(D.dtype, (int)D.d, q, prob->q_stride, D.b, D.hq, D.lq,
+                                         reinterpret_cast<float *>(keys_a) + g.side[si].base, sel->q_key, st), "norm_keys(q)"));
+      ++launches; ++si;
+    } else if (sel->q_key) {
+      BA_TRY(cuda_check(launch_norm_keys(D.dtype, (int)D.d, q, prob->q_stride, D.b, D.hq, D.lq, sel->q_key, nullptr, st), "norm_keys(q)"));
+      ++launches;
+    }
+    if (sort_k(pa)) {
+      g.side[si].perm_out = sel->perm_k;
+      BA_TRY(cuda_check(launch_norm_keys(D.dtype, (int)D.d, k, prob->k_stride, D.b, D.hkv, D.lk,
+                                         reinterpret_cast<float *>(keys_a) + g.side[si].base, sel->k_key, st), "norm_keys(k)"));
+      ++launches;
+    } else if (sel->k_key) {
+      BA_TRY(cuda_check(launch_norm_keys(D.dtype, (int)D.d, k, prob->k_stride, D.b, D.hkv, D.lk, sel->k_key, nullptr, st), "norm_keys(k)"));
+      ++launches;
+    }
+  }
+  // K2: stable segmented sort -> perm_q / perm_k
+  BA_TRY(cuda_check(launch_radix_sort(g, keys_a, vals_a, keys_b, vals_b, at<uint32_t>(ws, plan.hist), st, &launches), "radix_sort"));
+  // K3: permuted copies + block statistics
+  double *q_mean = sel->q_mean ? sel->q_mean : at<double>(ws, plan.q_mean);
+  double *q_var = sel->q_var ? sel->q_var : at<double>(ws, plan.q_var);
+  double *k_mean = sel->k_mean ? sel->k_mean : at<double>(ws, plan.k_mean);
+  double *k_var = sel->k_var ? sel->k_var : at<double>(ws, plan.k_var);
+  BA_TRY(cuda_check(launch_gather_stats(D.dtype, (int)D.d, q, prob->q_stride, D.b, D.hq, D.lq, (int)D.B,
+                                        sort_q(pa) ? sel->perm_q : nullptr, sort_q(pa) ? nullptr : sel->perm_q,
+                                        sel->q_sorted, q_mean, q_var, st), "gather_stats(q)"));
+  BA_TRY(cuda_check(launch_gather_stats(D.dtype, (int)D.d, k, prob->k_stride, D.b, D.hkv, D.lk, (int)D.B,
+                                        sort_k(pa) ? sel->perm_k : nullptr, sort_k(pa) ? nullptr : sel->perm_k,
+                                        sel->k_sorted, k_mean, k_var, st), "gather_stats(k)"));
+  BA_TRY(cuda_check(launch_gather_stats(D.dtype, (int)D.d, v, prob->v_stride, D.b, D.hkv, D.lk, (int)D.B,
+                                        sort_k(pa) ? sel->perm_k : nullptr, nullptr, sel->v_sorted, nullptr,
+                                        nullptr, st), "gather(v)"));
+  launches += 3;
+  // K4: scores, then per-row top-kappa
+  double *logits = sel->logits ? sel->logits : at<double>(ws, plan.logits);
+  BA_TRY(cuda_check(launch_scores((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, q_var, k_mean, k_var,
+                                  pa->comp == BA_COMP_DIAG ? 1 : 0, (double)pa->beta, logits, st), "scores"));
+  BA_TRY(cuda_check(launch_topk(D.b * D.hq * D.nq, D.nk, D.kappa, logits, sel->kv_index, sel->kv_count,
+                                sel->mask, sel->block_prob, sel->threshold, st), "topk"));
+  launches += 2;
+  g_launches = launches;
+  return BA_OK;
+}
+
+AttnArgs make_attn(const Dims &D, const ba_params *pa) {
+  AttnArgs a{};
+  a.dtype = D.dtype == BA_DTYPE_BF16 ? 0 : 1;
+  a.d = (int)D.d;
+  a.B = (int)D.B;
+  a.batch = D.b; a.hq = D.hq; a.hkv = D.hkv; a.lq = D.lq; a.lk = D.lk; a.nq = D.nq; a.nk = D.nk;
+  a.scale = pa->softmax_scale > 0.f ? pa->softmax_scale : (float)(1.0 / sqrt((double)D.d));
+  return a;
+}
+
+const char *attn_kernel_name(const AttnArgs &a) {
+  return attn_sm100_supported(a) ? "attn_sm100_tcgen05" : "attn_simt";
+}
+
+ba_status run_attn(const AttnArgs &a, cudaStream_t st) {
+  cudaError_t e;
+  if (attn_sm100_supported(a)) e = launch_attn_sm100(a, st);
+  else e = launch_attn_simt(a, st);
+  g_launches = 1;
+  return cuda_check(e, attn_kernel_name(a));
+}
+
+ba_status run_sparse(const Dims &D, const ba_problem *prob, const ba_params *pa, const ba_selection *sel,
+                     void *out, float *lse, cudaStream_t st) {
+  if (!sel) return fail(BA_ERR_INVALID_ARGUMENT, "selection is NULL");
+  BA_TRY(check_ptr("out", out));
+  BA_TRY(check_strides("o", prob->o_stride, D.esz));
+  BA_TRY(check_ptr("sel->q_sorted", sel->q_sorted));
+  BA_TRY(check_ptr("sel->k_sorted", sel->k_sorted));
+  BA_TRY(check_ptr("sel->v_sorted", sel->v_sorted));
+  if (!sel->kv_index || !sel->kv_count || !sel->perm_q)
+    return fail(BA_ERR_INVALID_ARGUMENT, "selection kv_index/kv_count/perm_q must be non-NULL");
+  AttnArgs a = make_attn(D, pa);
+  a.q = sel->q_sorted; a.k = sel->k_sorted; a.v = sel->v_sorted;
+  a.qs[0] = D.hq * D.lq * D.d; a.qs[1] = D.lq * D.d; a.qs[2] = D.d;
+  a.ks[0] = D.hkv * D.lk * D.d; a.ks[1] = D.lk * D.d; a.ks[2] = D.d;
+  for (int i = 0; i < 3; ++i) a.vs[i] = a.ks[i];
+  a.kv_index = sel->kv_index;
+  a.kv_count = sel->kv_count;
+  a.kv_stride = D.kappa;
+  a.perm_q = sel->perm_q;
+  a.out = out;
+  for (int i = 0; i < 3; ++i) a.os[i] = prob->o_stride[i];
+  a.lse = lse;
+  return run_attn(a, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ba_abi_version(void) { return BA_ABI_VERSION; }
+
+ba_status ba_selection_sizes(const ba_problem *prob, const ba_params *params, int64_t *kappa, int64_t *n_q,
+                             int64_t *n_k) {
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  if (kappa) *kappa = D.kappa;
+  if (n_q) *n_q = D.nq;
+  if (n_k) *n_k = D.nk;
+  return BA_OK;
+}
+
+size_t ba_select_workspace_size(const ba_problem *prob, const ba_params *params) {
+  Dims D;
+  if (check_problem(prob, params, &D) != BA_OK) return 0;
+  return plan_select(D, params, nullptr).total;
+}
+
+size_t ba_attention_workspace_size(const ba_problem *prob, const ba_params *params) {
+  Dims D;
+  if (check_problem(prob, params, &D) != BA_OK) return 0;
+  return plan_selbufs(D).total + plan_select(D, params, nullptr).total;
+}
+
+ba_status ba_select(const ba_problem *prob, const ba_params *params, const void *q, const void *k,
+                    const void *v, const ba_selection *sel, void *workspace, size_t workspace_bytes,
+                    cudaStream_t stream) {
+  g_err.clear();
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  return run_select(D, prob, params, q, k, v, sel, workspace, workspace_bytes, stream);
+}
+
+ba_status ba_sparse_attn(const ba_problem *prob, const ba_params *params, const ba_selection *sel, void *out,
+                         float *lse, cudaStream_t stream) {
+  g_err.clear();
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  return run_sparse(D, prob, params, sel, out, lse, stream);
+}
+
+ba_status ba_attention(const ba_problem *prob, const ba_params *params, const void *q, const void *k,
+                       const void *v, void *out, float *lse, void *workspace, size_t workspace_bytes,
+                       cudaStream_t stream) {
+  g_err.clear();
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  const SelBufPlan bp = plan_selbufs(D);
+  if (workspace_bytes < bp.total) return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu too small", workspace_bytes);
+  if (!workspace) return fail(BA_ERR_INVALID_ARGUMENT, "workspace is NULL");
+  ba_selection sel{};
+  sel.perm_q = at<int32_t>(workspace, bp.perm_q);
+  sel.perm_k = at<int32_t>(workspace, bp.perm_k);
+  sel.q_sorted = at<void>(workspace, bp.qs);
+  sel.k_sorted = at<void>(workspace, bp.ks);
+  sel.v_sorted = at<void>(workspace, bp.vs);
+  sel.kv_index = at<int32_t>(workspace, bp.kv_index);
+  sel.kv_count = at<int32_t>(workspace, bp.kv_count);
+  BA_TRY(run_select(D, prob, params, q, k, v, &sel, static_cast<char *>(workspace) + bp.total,
+                    workspace_bytes - bp.total, stream));
+  const int sel_launches = g_launches;
+  BA_TRY(run_sparse(D, prob, params, &sel, out, lse, stream));
+  g_launches += sel_launches;
+  return BA_OK;
+}
+
+ba_status ba_dense_attn(const ba_problem *prob, const ba_params *params, const void *q, const void *k,
+                        const void *v, void *out, float *lse, cudaStream_t stream) {
+  g_err.clear();
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  BA_TRY(check_ptr("q", q));
+  BA_TRY(check_ptr("k", k));
+  BA_TRY(check_ptr("v", v));
+  BA_TRY(check_ptr("out", out));
+  BA_TRY(check_strides("q", prob->q_stride, D.esz));
+  BA_TRY(check_strides("k", prob->k_stride, D.esz));
+  BA_TRY(check_strides("v", prob->v_stride, D.esz));
+  BA_TRY(check_strides("o", prob->o_stride, D.esz));
+  AttnArgs a = make_attn(D, params);
+  a.q = q; a.k = k; a.v = v;
+  for (int i = 0; i < 3; ++i) {
+    a.qs[i] = prob->q_stride[i]; a.ks[i] = prob->k_stride[i]; a.vs[i] = prob->v_stride[i]; a.os[i] = prob->o_stride[i];
+  }
+  a.kv_index = nullptr; a.kv_count = nullptr; a.kv_stride = D.nk; a.perm_q = nullptr;
+  a.out = out; a.lse = lse;
+  return run_attn(a, stream);
+}
+
+size_t ba_attention_host_workspace_size(const ba_problem *prob, const ba_params *params) {
+  Dims D;
+  if (check_problem(prob, params, &D) != BA_OK) return 0;
+  const size_t q = align_up(D.esz * D.b * D.hq * D.lq * D.d), kv = align_up(D.esz * D.b * D.hkv * D.lk * D.d);
+  return 2 * q + 2 * kv + ba_attention_workspace_size(prob, params);
+}
+
+ba_status ba_attention_host(const ba_problem *prob, const ba_params *params, const void *q_host,
+                            const void *k_host, const void *v_host, void *out_host, void *workspace,
+                            size_t workspace_bytes, cudaStream_t stream) {
+  g_err.clear();
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  if (!q_host || !k_host || !v_host || !out_host) return fail(BA_ERR_INVALID_ARGUMENT, "host pointer is NULL");
+  if (!workspace) return fail(BA_ERR_INVALID_ARGUMENT, "workspace is NULL");
+  const size_t need = ba_attention_host_workspace_size(prob, params);
+  if (workspace_bytes < need) return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu < %zu", workspace_bytes, need);
+  const size_t qb = D.esz * D.b * D.hq * D.lq * D.d, kvb = D.esz * D.b * D.hkv * D.lk * D.d;
+  char *w = static_cast<char *>(workspace);
+  void *qd = w; w += align_up(qb);
+  void *kd = w; w += align_up(kvb);
+  void *vd = w; w += align_up(kvb);
+  void *od = w; w += align_up(qb);
+  BA_TRY(cuda_check(cudaMemcpyAsync(qd, q_host, qb, cudaMemcpyHostToDevice, stream), "H2D q"));
+  BA_TRY(cuda_check(cudaMemcpyAsync(kd, k_host, kvb, cudaMemcpyHostToDevice, stream), "H2D k"));
+  BA_TRY(cuda_check(cudaMemcpyAsync(vd, v_host, kvb, cudaMemcpyHostToDevice, stream), "H2D v"));
+  ba_problem p = *prob;
+  p.q_stride[2] = D.d; p.q_stride[1] = D.lq * D.d; p.q_stride[0] = D.hq * D.lq * D.d;
+  p.o_stride[0] = p.q_stride[0]; p.o_stride[1] = p.q_stride[1]; p.o_stride[2] = p.q_stride[2];
+  p.k_stride[2] = D.d; p.k_stride[1] = D.lk * D.d; p.k_stride[0] = D.hkv * D.lk * D.d;
+  for (int i = 0; i < 3; ++i) p.v_stride[i] = p.k_stride[i];
+  BA_TRY(ba_attention(&p, params, qd, kd, vd, od, nullptr, w, workspace_bytes - (size_t)(w - static_cast<char *>(workspace)), stream));
+  BA_TRY(cuda_check(cudaMemcpyAsync(out_host, od, qb, cudaMemcpyDeviceToHost, stream), "D2H out"));
+  return BA_OK;
+}
+
+int ba_last_launch_count(void) { return g_launches; }
+
+const char *ba_attention_kernel_name(const ba_problem *prob, const ba_params *params) {
+  Dims D;
+  if (check_problem(prob, params, &D) != BA_OK) return "";
+  return attn_kernel_name(make_attn(D, params));
+}
+
+const char *ba_status_string(ba_status s) {
+  switch (s) {
+    case BA_OK: return "BA_OK";
+    case BA_ERR_INVALID_ARGUMENT: return "BA_ERR_INVALID_ARGUMENT";
+    case BA_ERR_SHAPE_MISMATCH: return "BA_ERR_SHAPE_MISMATCH";
+    case BA_ERR_UNSUPPORTED: return "BA_ERR_UNSUPPORTED";
+    case BA_ERR_WORKSPACE_TOO_SMALL: return "BA_ERR_WORKSPACE_TOO_SMALL";
+    case BA_ERR_CUDA: return "BA_ERR_CUDA";
+    case BA_ERR_EMPTY_MASK_ROW: return "BA_ERR_EMPTY_MASK_ROW";
+  }
+  return "BA_ERR_UNKNOWN";
+}
+
+const char *ba_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

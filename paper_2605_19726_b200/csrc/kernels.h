@@ -1,0 +1,78 @@
+// kernels.h — internal launch interface between api.cu and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace baatt {
+
+// ---------------------------------------------------------------- sort geometry
+// A "side" is Q or K.  Every (batch, head) row of length L is split into
+// windows of `win` tokens (win = L for the global sort); every window is one
+// independently sorted segment; every segment is cut into tiles of kSortTile.
+constexpr int kSortThreads = 256;
+constexpr int kSortIPT = 16;
+constexpr int kSortTile = kSortThreads * kSortIPT;  // 4096 keys per tile
+
+struct SortSide {
+  int64_t heads = 0;          // batch * H
+  int64_t L = 0;
+  int64_t win = 0;            // window length (== L for global)
+  int64_t n_win = 0;          // ceil(L / win)
+  int64_t tiles_per_win = 0;  // ceil(win / kSortTile)
+  int64_t base = 0;           // element offset of this side in the combined key buffer
+  int64_t tile_base = 0;      // first global tile id of this side
+  int64_t seg_base = 0;       // first global segment id of this side
+  int32_t *perm_out = nullptr;
+  int64_t tiles() const { return heads * n_win * tiles_per_win; }
+  int64_t segs() const { return heads * n_win; }
+};
+
+struct SortGeom {
+  SortSide side[2];
+  int n_sides = 0;
+  int64_t tiles_total = 0;
+  int64_t segs_total = 0;
+  int64_t keys_total = 0;
+};
+
+// ---------------------------------------------------------------- K1 .. K4
+// dtype: 0 = bf16, 1 = fp32
+cudaError_t launch_norm_keys(int dtype, int d, const void *x, const int64_t *stride, int64_t batch,
+                             int64_t heads, int64_t L, float *keys, float *keys_user,
+                             cudaStream_t st);
+cudaError_t launch_radix_sort(const SortGeom &g, uint32_t *keys_a, uint32_t *vals_a, uint32_t *keys_b,
+                              uint32_t *vals_b, uint32_t *hist, cudaStream_t st, int *launches);
+cudaError_t launch_gather_stats(int dtype, int d, const void *x, const int64_t *stride, int64_t batch,
+                                int64_t heads, int64_t L, int B, const int32_t *perm,
+                                int32_t *perm_identity_out, void *xs, double *mean, double *var,
+                                cudaStream_t st);
+cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk,
+                          const double *q_mean, const double *q_var, const double *k_mean,
+                          const double *k_var, int comp, double beta, double *logits,
+                          cudaStream_t st);
+cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, const double *logits,
+                        int32_t *kv_index, int32_t *kv_count, uint8_t *mask, double *prob,
+                        double *tau, cudaStream_t st);
+
+// ---------------------------------------------------------------- attention
+struct AttnArgs {
+  int dtype;          // 0 bf16, 1 fp32
+  int d;              // head dim
+  int B;              // block size
+  int64_t batch, hq, hkv, lq, lk, nq, nk;
+  const void *q, *k, *v;       // (sorted) inputs
+  int64_t qs[3], ks[3], vs[3]; // element strides (batch, head, token)
+  const int32_t *kv_index;     // [b, hq, nq, kv_stride] or nullptr = all blocks
+  const int32_t *kv_count;     // [b, hq, nq] or nullptr = kappa
+  int64_t kv_stride;           // row stride of kv_index (== kappa)
+  const int32_t *perm_q;       // [b, hq, lq] or nullptr = identity
+  void *out;
+  int64_t os[3];
+  float *lse;                  // [b, hq, lq] or nullptr
+  float scale;
+};
+cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t st);
+cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st);
+bool attn_sm100_supported(const AttnArgs &a);
+
+}  // namespace baatt

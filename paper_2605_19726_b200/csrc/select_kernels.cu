@@ -1,0 +1,577 @@
+// select_kernels.cu — BA-Att pattern selection on sm_100a (Alg. 1 steps 1-10,
+// PAPER.md P:535-562).
+//
+//   K1 norm_keys     key = fp32(||x||^2) per Q / K row (reading A4):
+//                    HBM-bound, one half-warp per row, 128-bit loads, fp64
+//                    partial sums combined by an xor-shuffle tree.
+//   K2 radix sort    stable ascending argsort of the keys per (batch, head,
+//                    window) segment (ties -> lower index):
+//                    LSD radix, 4 x 8-bit passes, each = tile histogram +
+//                    per-segment scan + stable tile scatter staged in smem.
+//   K3 gather_stats  Q' = Q[pi_q], K' = K[pi_k], V' = V[pi_k]
+//                    plus per-block mean and population variance (P:282,
+//                    P:516) in fp64 from the same registers:
+//                    HBM-bound, one CTA per block, coalesced 128-bit rows.
+//   K4a scores       l' = Qbar.Kbar/sqrt(d) + (beta/d) sum_t (VarQ Kbar^2 +
+//                    VarK Qbar^2 + VarQ VarK) (Eq. block-logit P:286-287,
+//                    Eq. diag-variance-form) as ONE
+//                    inner product of length 3d between the features
+//                    Xq = [Qbar/sqrt(d), (beta/d)VarQ, (beta/d)Qbar^2] and
+//                    Xk = [Kbar, Kbar^2 + VarK, VarK]: an fp64 SIMT micro-GEMM
+//                    (64x64 tiles, 4x4 per thread) — fp64 so that masks match
+//                    the fp64 oracle.
+//   K4b topk         per row: max, optional m' = softmax(l'),
+//                    exact kappa-th largest l' by a 64-step radix select on
+//                    order-preserving bits, ties -> lower g_k, ascending index
+//                    list + mask.  One warp per row, row in smem.
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace baatt {
+
+// =====================================================================================
+// K1: norm keys.  One half-warp (16 lanes) per row; lane l owns features
+// [l*d/16, (l+1)*d/16) and sums their squares sequentially in fp64; the 16
+// partial sums are combined with xor offsets 8, 4, 2, 1 (a+b == b+a exactly,
+// so every lane of a pair holds the oracle's p[l] + p[l+8], ...).
+// =====================================================================================
+template <typename T, int D>
+__global__ void __launch_bounds__(256) norm_keys_kernel(const T *__restrict__ x, int64_t s0, int64_t s1,
+                                                        int64_t s2, int64_t heads, int64_t L,
+                                                        float *__restrict__ keys,
+                                                        float *__restrict__ keys_user) {
+  constexpr int PER_LANE = D / 16;  // 4 or 8 elements
+  const int lane16 = threadIdx.x & 15;
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 4;
+  const int64_t total = int64_t(gridDim.y) * heads * L;  // gridDim.y = batch
+  (void)total;
+  const int64_t bh_rows = heads * L;
+  const int64_t b = blockIdx.y;
+  if (row >= bh_rows) return;  // whole half-warps exit together
+  const int64_t h = row / L, t = row - h * L;
+  const T *p = x + b * s0 + h * s1 + t * s2 + lane16 * PER_LANE;
+  float f[PER_LANE];
+  if constexpr (sizeof(T) * PER_LANE == 16) {
+    uint4 u = ldg16(p);
+    Chunk<T>::unpack(u, *reinterpret_cast<float(*)[16 / sizeof(T)]>(f));
+  } else if constexpr (sizeof(T) * PER_LANE == 32) {
+    float a[4], c[4];
+    Chunk<T>::unpack(ldg16(p), a);
+    Chunk<T>::unpack(ldg16(p + 4), c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { f[i] = a[i]; f[4 + i] = c[i]; }
+  } else {  // bf16, d = 64: 8 bytes
+    uint2 u = __ldg(reinterpret_cast<const uint2 *>(p));
+    f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xffff0000u);
+    f[2] = __uint_as_float(u.y << 16); f[3] = __uint_as_float(u.y & 0xffff0000u);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < PER_LANE; ++i) {
+    const double v = static_cast<double>(f[i]);
+    s = fma(v, v, s);  // v*v is exact in fp64, so fma == mul-then-add
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 8);
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  if (lane16 == 0) {
+    const float k = __double2float_rn(s);
+    const int64_t o = b * bh_rows + row;
+    keys[o] = k;
+    if (keys_user) keys_user[o] = k;
+  }
+}
+
+cudaError_t launch_norm_keys(int dtype, int d, const void *x, const int64_t *st, int64_t batch,
+                             int64_t heads, int64_t L, float *keys, float *keys_user,
+                             cudaStream_t stream) {
+  const int64_t rows = heads * L;
+  dim3 grid((unsigned)((rows * 16 + 255) / 256), (unsigned)batch);
+  if (dtype == 0 && d == 128)
+    norm_keys_kernel<__nv_bfloat16, 128><<<grid, 256, 0, stream>>>((const __nv_bfloat16 *)x, st[0], st[1], st[2], heads, L, keys, keys_user);
+  else if (dtype == 0 && d == 64)
+    norm_keys_kernel<__nv_bfloat16, 64><<<grid, 256, 0, stream>>>((const __nv_bfloat16 *)x, st[0], st[1], st[2], heads, L, keys, keys_user);
+  else if (dtype == 1 && d == 128)
+    norm_keys_kernel<float, 128><<<grid, 256, 0, stream>>>((const float *)x, st[0], st[1], st[2], heads, L, keys, keys_user);
+  else
+    norm_keys_kernel<float, 64><<<grid, 256, 0, stream>>>((const float *)x, st[0], st[1], st[2], heads, L, keys, keys_user);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K2: segmented stable LSD radix sort.
+// =====================================================================================
+struct TileLoc {
+  int side;
+  int64_t seg;        // global segment id
+  int64_t seg_start;  // element offset of the segment in the combined buffer
+  int64_t seg_len;
+  int64_t tile_off;   // offset of this tile inside the segment
+  int64_t count;      // items in this tile (may be <= 0 for empty tail tiles)
+  int64_t head;       // (batch*H) index within the side
+  int64_t win_start;  // token index of the window start inside the head row
+};
+
+BA_DEVICE TileLoc locate_tile(const SortGeom &g, int64_t t) {
+  TileLoc r;
+  int s = (g.n_sides == 2 && t >= g.side[1].tile_base) ? 1 : 0;
+  const SortSide &sd = g.side[s];
+  const int64_t lt = t - sd.tile_base;
+  const int64_t per_head = sd.n_win * sd.tiles_per_win;
+  const int64_t head = lt / per_head;
+  const int64_t rem = lt - head * per_head;
+  const int64_t w = rem / sd.tiles_per_win;
+  const int64_t tw = rem - w * sd.tiles_per_win;
+  r.side = s;
+  r.head = head;
+  r.seg = sd.seg_base + head * sd.n_win + w;
+  r.win_start = w * sd.win;
+  r.seg_start = sd.base + head * sd.L + r.win_start;
+  r.seg_len = imin64(sd.win, sd.L - r.win_start);
+  r.tile_off = tw * kSortTile;
+  r.count = imin64(kSortTile, r.seg_len - r.tile_off);
+  return r;
+}
+
+// Per-tile 256-bin histogram of digit `shift`.
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(SortGeom g, const uint32_t *__restrict__ keys,
+                                                                  uint32_t *__restrict__ hist, int shift) {
+  __shared__ uint32_t h[256];
+  const int64_t t = blockIdx.x;
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const TileLoc loc = locate_tile(g, t);
+  const uint32_t *src = keys + loc.seg_start + loc.tile_off;
+  for (int64_t i = threadIdx.x; i < loc.count; i += kSortThreads)
+    atomicAdd(&h[(__ldg(src + i) >> shift) & 255u], 1u);
+  __syncthreads();
+  hist[t * 256 + threadIdx.x] = h[threadIdx.x];
+}
+
+// Per segment: offsets[tile][digit] = sum_{d' < digit} total(d') + sum_{tile' < tile} count(tile', digit)
+// (digit-major order => stable).  One CTA of 256 threads per segment; thread = digit.
+__global__ void __launch_bounds__(256) radix_scan_kernel(SortGeom g, uint32_t *__restrict__ hist) {
+  __shared__ uint32_t tot[256];
+  const int64_t seg = blockIdx.x;
+  const int s = (g.n_sides == 2 && seg >= g.side[1].seg_base) ? 1 : 0;
+  const SortSide &sd = g.side[s];
+  const int64_t tile0 = sd.tile_base + (seg - sd.seg_base) * sd.tiles_per_win;
+  const int digit = threadIdx.x;
+  uint32_t run = 0;
+  for (int64_t i = 0; i < sd.tiles_per_win; ++i) {
+    uint32_t c = hist[(tile0 + i) * 256 + digit];
+    hist[(tile0 + i) * 256 + digit] = run;  // exclusive within digit
+    run += c;
+  }
+  tot[digit] = run;
+  __syncthreads();
+  // exclusive scan of tot over digits (Hillis-Steele in smem; 256 entries)
+  uint32_t v = tot[digit];
+  for (int off = 1; off < 256; off <<= 1) {
+    __syncthreads();
+    uint32_t a = digit >= off ? tot[digit - off] : 0u;
+    __syncthreads();
+    tot[digit] += a;
+  }
+  __syncthreads();
+  const uint32_t base = tot[digit] - v;
+  for (int64_t i = 0; i < sd.tiles_per_win; ++i) hist[(tile0 + i) * 256 + digit] += base;
+}
+
+// Stable scatter of one tile.  Warp w owns tile items [w*512, (w+1)*512); in
+// round r lane l holds item w*512 + r*32 + l.  Rank of an item among equal
+// digits = (items of earlier warps) + (earlier rounds of this warp) +
+// (lower lanes of this round) — exactly the original order within the tile.
+template <bool kFirst, bool kLast>
+__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
+    SortGeom g, const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+    uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, const uint32_t *__restrict__ offsets,
+    int shift) {
+  constexpr int kWarps = kSortThreads / 32;
+  constexpr int kPerWarp = kSortTile / kWarps;  // 512
+  __shared__ uint32_t wcount[kWarps][256];
+  __shared__ uint32_t dstart[256];
+  __shared__ uint32_t s_off[256];
+  __shared__ uint32_t s_keys[kSortTile];
+  __shared__ uint32_t s_vals[kSortTile];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x;
+  const TileLoc loc = locate_tile(g, t);
+  if (loc.count <= 0) return;  // uniform across the CTA
+  for (int i = threadIdx.x; i < kWarps * 256; i += kSortThreads) (&wcount[0][0])[i] = 0;
+  s_off[threadIdx.x] = offsets[t * 256 + threadIdx.x];
+  __syncthreads();
+
+  const int64_t base = loc.seg_start + loc.tile_off;
+  uint32_t key[kSortIPT], val[kSortIPT], rank[kSortIPT];
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r) {
+    const int item = warp * kPerWarp + r * 32 + lane;
+    const bool valid = item < loc.count;
+    key[r] = valid ? keys_in[base + item] : 0xffffffffu;
+    if constexpr (kFirst) val[r] = (uint32_t)(loc.win_start + loc.tile_off + item);
+    else val[r] = valid ? vals_in[base + item] : 0u;
+    const uint32_t digit = (key[r] >> shift) & 255u;
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    rank[r] = 0;
+    if (valid) {
+      const unsigned peers = __match_any_sync(vmask, digit);
+      const uint32_t before = wcount[warp][digit];
+      rank[r] = before + __popc(peers & lt);
+      // the highest peer lane publishes the new count after all peers read it
+      __syncwarp(vmask);
+      if ((peers >> lane) == 1u) wcount[warp][digit] = before + __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  {  // per digit: exclusive over warps, then tile totals
+    const int dg = threadIdx.x;
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = wcount[w][dg];
+      wcount[w][dg] = run;
+      run += c;
+    }
+    dstart[dg] = run;
+  }
+  __syncthreads();
+  {  // exclusive scan of tile digit totals -> dstart
+    const int dg = threadIdx.x;
+    const uint32_t v = dstart[dg];
+    for (int off = 1; off < 256; off <<= 1) {
+      __syncthreads();
+      const uint32_t a = dg >= off ? dstart[dg - off] : 0u;
+      __syncthreads();
+      dstart[dg] += a;
+    }
+    __syncthreads();
+    dstart[dg] -= v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r) {
+    const int item = warp * kPerWarp + r * 32 + lane;
+    if (item < loc.count) {
+      const uint32_t digit = (key[r] >> shift) & 255u;
+      const uint32_t pos = dstart[digit] + wcount[warp][digit] + rank[r];
+      s_keys[pos] = key[r];
+      s_vals[pos] = val[r];
+    }
+  }
+  __syncthreads();
+  // coalesced write-out: runs of equal digits go to consecutive global slots
+  for (int i = threadIdx.x; i < loc.count; i += kSortThreads) {
+    const uint32_t k = s_keys[i];
+    const uint32_t digit = (k >> shift) & 255u;
+    const int64_t gpos = s_off[digit] + (i - dstart[digit]);
+    if constexpr (kLast) {
+      const SortSide &sd = g.side[loc.side];
+      sd.perm_out[loc.head * sd.L + loc.win_start + gpos] = (int32_t)s_vals[i];
+    } else {
+      keys_out[loc.seg_start + gpos] = k;
+      vals_out[loc.seg_start + gpos] = s_vals[i];
+    }
+  }
+}
+
+cudaError_t launch_radix_sort(const SortGeom &g, uint32_t *keys_a, uint32_t *vals_a, uint32_t *keys_b,
+                              uint32_t *vals_b, uint32_t *hist, cudaStream_t st, int *launches) {
+  if (g.tiles_total == 0) return cudaSuccess;
+  uint32_t *kin = keys_a, *vin = vals_a, *kout = keys_b, *vout = vals_b;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = pass * 8;
+    radix_hist_kernel<<<(unsigned)g.tiles_total, kSortThreads, 0, st>>>(g, kin, hist, shift);
+    radix_scan_kernel<<<(unsigned)g.segs_total, 256, 0, st>>>(g, hist);
+    if (pass == 0)
+      radix_scatter_kernel<true, false><<<(unsigned)g.tiles_total, kSortThreads, 0, st>>>(g, kin, vin, kout, vout, hist, shift);
+    else if (pass == 3)
+      radix_scatter_kernel<false, true><<<(unsigned)g.tiles_total, kSortThreads, 0, st>>>(g, kin, vin, kout, vout, hist, shift);
+    else
+      radix_scatter_kernel<false, false><<<(unsigned)g.tiles_total, kSortThreads, 0, st>>>(g, kin, vin, kout, vout, hist, shift);
+    *launches += 3;
+    uint32_t *tk = kin, *tv = vin;
+    kin = kout; vin = vout; kout = tk; vout = tv;
+  }
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K3: gather rows through pi and compute per-block mean / population variance.
+// One CTA (256 threads) per (block g, batch*head).  A thread owns one 16-byte
+// chunk (EPC features) of rows r0, r0 + RPI, ...; the block's rows stay in
+// registers between the copy, the mean pass and the variance pass.
+// =====================================================================================
+template <typename T, int D>
+__global__ void __launch_bounds__(256) gather_stats_kernel(
+    const T *__restrict__ x, int64_t s0, int64_t s1, int64_t s2, int64_t heads, int64_t L, int B,
+    const int32_t *__restrict__ perm, int32_t *__restrict__ perm_id_out, T *__restrict__ xs,
+    double *__restrict__ mean, double *__restrict__ var) {
+  constexpr int EPC = Chunk<T>::EPC;
+  constexpr int CPR = D / EPC;       // chunks per row
+  constexpr int RPI = 256 / CPR;     // rows per iteration
+  constexpr int MAXIT = 128 / RPI;   // B <= 128
+  __shared__ double red[RPI][D + 1];
+  __shared__ double s_mean[D];
+  const int64_t g = blockIdx.x;
+  const int64_t bh = blockIdx.y;  // batch * heads + head
+  const int64_t b = bh / heads, h = bh - b * heads;
+  const int chunk = threadIdx.x % CPR;
+  const int rsub = threadIdx.x / CPR;
+  const int64_t row0 = g * B;
+  const int n = (int)imin64(B, L - row0);
+  const T *xbase = x + b * s0 + h * s1 + chunk * EPC;
+  T *xsbase = xs + (bh * L + row0) * D + chunk * EPC;
+  float vals[MAXIT][EPC];
+  double acc[EPC];
+#pragma unroll
+  for (int e = 0; e < EPC; ++e) acc[e] = 0.0;
+#pragma unroll
+  for (int it = 0; it < MAXIT; ++it) {
+    const int r = rsub + it * RPI;
+    if (r < n) {
+      const int64_t tok = row0 + r;
+      int64_t src = tok;
+      if (perm) src = __ldg(perm + bh * L + tok);
+      else if (perm_id_out && chunk == 0) perm_id_out[bh * L + tok] = (int32_t)tok;
+      const uint4 u = ldg16(xbase + src * s2);
+      stg16(xsbase + (int64_t)r * D, u);
+      Chunk<T>::unpack(u, vals[it]);
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) acc[e] += (double)vals[it][e];
+    }
+  }
+  if (!mean) return;  // V: copy only
+#pragma unroll
+  for (int e = 0; e < EPC; ++e) red[rsub][chunk * EPC + e] = acc[e];
+  __syncthreads();
+  const double inv_n = 1.0 / (double)n;
+  for (int c = threadIdx.x; c < D; c += 256) {
+    double s = 0.0;
+    for (int i = 0; i < RPI; ++i) s += red[i][c];
+    s_mean[c] = s * inv_n;
+  }
+  __syncthreads();
+  double mu[EPC];
+#pragma unroll
+  for (int e = 0; e < EPC; ++e) { mu[e] = s_mean[chunk * EPC + e]; acc[e] = 0.0; }
+#pragma unroll
+  for (int it = 0; it < MAXIT; ++it) {
+    const int r = rsub + it * RPI;
+    if (r < n) {
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) {
+        const double dv = (double)vals[it][e] - mu[e];
+        acc[e] = fma(dv, dv, acc[e]);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < EPC; ++e) red[rsub][chunk * EPC + e] = acc[e];
+  __syncthreads();
+  const int64_t nb = (L + B - 1) / B;
+  for (int c = threadIdx.x; c < D; c += 256) {
+    double s = 0.0;
+    for (int i = 0; i < RPI; ++i) s += red[i][c];
+    mean[(bh * nb + g) * D + c] = s_mean[c];
+    var[(bh * nb + g) * D + c] = s * inv_n;
+  }
+}
+
+cudaError_t launch_gather_stats(int dtype, int d, const void *x, const int64_t *st, int64_t batch,
+                                int64_t heads, int64_t L, int B, const int32_t *perm,
+                                int32_t *perm_id_out, void *xs, double *mean, double *var,
+                                cudaStream_t stream) {
+  dim3 grid((unsigned)((L + B - 1) / B), (unsigned)(batch * heads));
+#define BA_GS(T, D) gather_stats_kernel<T, D><<<grid, 256, 0, stream>>>((const T *)x, st[0], st[1], st[2], heads, L, B, perm, perm_id_out, (T *)xs, mean, var)
+  if (dtype == 0 && d == 128) BA_GS(__nv_bfloat16, 128);
+  else if (dtype == 0 && d == 64) BA_GS(__nv_bfloat16, 64);
+  else if (dtype == 1 && d == 128) BA_GS(float, 128);
+  else BA_GS(float, 64);
+#undef BA_GS
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K4a: compensated block logits as an fp64 micro-GEMM over 3d features.
+// =====================================================================================
+constexpr int kScTile = 64;
+constexpr int kScK = 16;
+
+template <int D>
+__global__ void __launch_bounds__(256) scores_kernel(int64_t hq, int64_t grp, int64_t nq, int64_t nk,
+                                                     const double *__restrict__ q_mean,
+                                                     const double *__restrict__ q_var,
+                                                     const double *__restrict__ k_mean,
+                                                     const double *__restrict__ k_var, int comp,
+                                                     double inv_sqrt_d, double beta_over_d,
+                                                     double *__restrict__ logits) {
+  __shared__ double As[kScK][kScTile + 2];
+  __shared__ double Bs[kScK][kScTile + 2];
+  const int64_t bhq = blockIdx.z;            // batch * hq + head
+  const int64_t b = bhq / hq, h = bhq - b * hq;
+  const int64_t bhk = b * (hq / grp) + h / grp;
+  const int64_t gq0 = (int64_t)blockIdx.y * kScTile, gk0 = (int64_t)blockIdx.x * kScTile;
+  const double *qm = q_mean + bhq * nq * D, *qv = q_var + bhq * nq * D;
+  const double *km = k_mean + bhk * nk * D, *kv = k_var + bhk * nk * D;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  const int nfeat = comp ? 3 * D : D;
+  for (int c0 = 0; c0 < nfeat; c0 += kScK) {
+    // load 64 rows x 16 features of each side; thread -> (row = tid/4, 4 features)
+    {
+      const int r = threadIdx.x >> 2, f0 = (threadIdx.x & 3) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = c0 + f0 + e;
+        const int part = c / D, t = c - part * D;
+        const int64_t gq = gq0 + r, gk = gk0 + r;
+        double a = 0.0, bb = 0.0;
+        if (gq < nq) {
+          const double m = qm[gq * D + t];
+          a = part == 0 ? m * inv_sqrt_d : part == 1 ? beta_over_d * qv[gq * D + t] : beta_over_d * (m * m);
+        }
+        if (gk < nk) {
+          const double m = km[gk * D + t];
+          bb = part == 0 ? m : part == 1 ? fma(m, m, kv[gk * D + t]) : kv[gk * D + t];
+        }
+        As[f0 + e][r] = a;
+        Bs[f0 + e][r] = bb;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScK; ++k) {
+      double a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = As[k][ty * 4 + i]; bb[i] = Bs[k][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gq = gq0 + ty * 4 + i;
+    if (gq >= nq) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gk = gk0 + tx * 4 + j;
+      if (gk < nk) logits[(bhq * nq + gq) * nk + gk] = acc[i][j];
+    }
+  }
+}
+
+cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk,
+                          const double *q_mean, const double *q_var, const double *k_mean,
+                          const double *k_var, int comp, double beta, double *logits,
+                          cudaStream_t st) {
+  dim3 grid((unsigned)((nk + kScTile - 1) / kScTile), (unsigned)((nq + kScTile - 1) / kScTile),
+            (unsigned)(batch * hq));
+  const double inv_sqrt_d = 1.0 / sqrt((double)d), bod = beta / (double)d;
+  const int64_t grp = hq / hkv;
+  if (d == 128)
+    scores_kernel<128><<<grid, 256, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits);
+  else
+    scores_kernel<64><<<grid, 256, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K4b: per-row top-kappa.  One warp per row; the row's l' values sit in smem.
+// =====================================================================================
+__global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, const double *__restrict__ logits,
+                            int32_t *__restrict__ kv_index, int32_t *__restrict__ kv_count,
+                            uint8_t *__restrict__ mask, double *__restrict__ prob,
+                            double *__restrict__ tau) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (row >= rows) return;
+  double *x = reinterpret_cast<double *>(smem_raw) + (int64_t)warp * nk;
+  const double *src = logits + row * nk;
+  double mx = -INFINITY;
+  for (int64_t j = lane; j < nk; j += 32) {
+    const double v = src[j];
+    x[j] = v;
+    mx = fmax(mx, v);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  __syncwarp();
+  double denom = 0.0;
+  const bool need_prob = (prob != nullptr) || (tau != nullptr);
+  if (need_prob) {
+    for (int64_t j = lane; j < nk; j += 32) denom += exp(x[j] - mx);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, off);
+    if (prob)
+      for (int64_t j = lane; j < nk; j += 32) prob[row * nk + j] = exp(x[j] - mx) / denom;
+  }
+  // kappa-th largest ordered key: greedy MSB-first, keep the largest prefix T
+  // with #(u >= T) >= kappa.
+  uint64_t T = 0;
+  for (int bit = 63; bit >= 0; --bit) {
+    const uint64_t cand = T | (1ull << bit);
+    unsigned cnt = 0;
+    for (int64_t j = lane; j < nk; j += 32) cnt += ordered_bits(x[j]) >= cand;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (cnt >= (unsigned)kappa) T = cand;
+  }
+  unsigned gt = 0;
+  for (int64_t j = lane; j < nk; j += 32) gt += ordered_bits(x[j]) > T;
+  gt = __reduce_add_sync(0xffffffffu, gt);
+  const unsigned need_eq = (unsigned)kappa - gt;  // >= 1
+  unsigned eq_seen = 0, sel_seen = 0;
+  const unsigned lt = lanemask_lt();
+  for (int64_t j0 = 0; j0 < nk; j0 += 32) {
+    const int64_t j = j0 + lane;
+    bool sel = false, eq = false;
+    if (j < nk) {
+      const uint64_t u = ordered_bits(x[j]);
+      eq = (u == T);
+      sel = u > T;
+    }
+    const unsigned eqm = __ballot_sync(0xffffffffu, eq);
+    if (eq) sel = (eq_seen + __popc(eqm & lt)) < need_eq;
+    const unsigned selm = __ballot_sync(0xffffffffu, sel);
+    if (sel) kv_index[row * kappa + sel_seen + __popc(selm & lt)] = (int32_t)j;
+    if (mask && j < nk) mask[row * nk + j] = sel ? 1 : 0;
+    eq_seen += __popc(eqm);
+    sel_seen += __popc(selm);
+  }
+  if (lane == 0) kv_count[row] = (int32_t)kappa;
+  if (tau && lane == 0) {
+    // invert the order-preserving map: T holds the kappa-th largest l' exactly
+    const uint64_t u = (T >> 63) ? (T ^ 0x8000000000000000ull) : ~T;
+    tau[row] = exp(__longlong_as_double((long long)u) - mx) / denom;
+  }
+}
+
+cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, const double *logits, int32_t *kv_index,
+                        int32_t *kv_count, uint8_t *mask, double *prob, double *tau, cudaStream_t st) {
+  int warps = 8;
+  while (warps > 1 && (size_t)warps * nk * sizeof(double) > 160 * 1024) warps >>= 1;
+  const size_t smem = (size_t)warps * nk * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const unsigned grid = (unsigned)((rows + warps - 1) / warps);
+  topk_kernel<<<grid, warps * 32, smem, st>>>(rows, nk, kappa, logits, kv_index, kv_count, mask, prob, tau);
+  return cudaGetLastError();
+}
+
+}  // namespace baatt
