@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""bench.py — BA-Att hot path on B200: block-sparse attention TFLOP/s at 50%
+block sparsity (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C|A|V|M|T]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+    python bench.py --impl reference ...                   (the CPU oracle arm)
+
+A step = one pass of the whole hot path over one batch of synthetic input:
+ba_select (Alg. 1 steps 1-10: norm keys, sort, permute + block stats, scores,
+top-kappa) + ba_sparse_attn (steps 11-12: tcgen05 block-sparse attention,
+un-permute).  `value` = algorithmic FLOPs of the selected block pairs
+(4 n_q n_k d per pair, ragged sizes exact) summed over ranks / the max over
+ranks of the device time.  Scaling is weak: each rank processes its own batch
+element of the workload (heads and batch are independent; no collective on the
+data path).  Inputs (1.6 GB per step at config C) are larger than L2 (126 MB).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "block-sparse attn TFLOP/s & speedup vs dense at 50% sparsity, L=32K–128K"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C")
+    ap.add_argument("--density", type=float, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / e2e / cpu legs)")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"tflops_burst": d.get("bf16_tflops"), "tflops_sustained": d.get("bf16_tflops_sustained"),
+                "hbm_gbs": d.get("hbm_gbs"), "source": "measured"}
+    return {"tflops_burst": 1590.0, "tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def workload_desc(w, density):
+    return (f"{w.name} (config {w.config_index}): per rank b=1, Hq={w.heads_q}, Hkv={w.heads_kv}, "
+            f"L={w.seq_len}, d={w.head_dim}, B={w.block_size}, density={density} "
+            f"({int(round((1 - density) * 100))}% block sparsity), sort=qk, comp=diag, beta=1")
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits", "-lms", "200"],
+                                     stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+                except ValueError:
+                    pass
+        os.unlink(self.path)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        sm = sorted(r[0] for r in rows)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- FLOPs
+def sparse_flops_from_index(kv_index, kv_count, lq, lk, B, d):
+    """Sum over selected pairs of 4 n_q n_k d (QK^T + PV), ragged sizes exact."""
+    import torch
+    nq = kv_index.shape[2]
+    nk_tot = (lk + B - 1) // B
+    last_k = lk - (nk_tot - 1) * B
+    nq_rows = torch.full((nq,), B, dtype=torch.float64, device=kv_index.device)
+    nq_rows[-1] = lq - (nq - 1) * B
+    kap = kv_index.shape[3]
+    valid = torch.arange(kap, device=kv_index.device)[None, None, None, :] < kv_count[..., None]
+    nk_sizes = torch.where(kv_index == nk_tot - 1, float(last_k), float(B)).double() * valid
+    per_row = nk_sizes.sum(-1)  # [b, h, nq]
+    return float((per_row * nq_rows[None, None, :]).sum().item()) * 4.0 * d
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
+# --------------------------------------------------------------------------- oracle sample
+def oracle_sample(w, q, k, v, density, n_blocks, seed=0):
+    """Run the fp64 oracle on a bounded sample of the workload: the full
+    selection (Alg. 1 steps 1-10) of one q-head and block-sparse attention
+    for `n_blocks` of its query blocks.  Returns (flops, seconds, desc)."""
+    import numpy as np
+    import oracle as O
+    t0 = time.perf_counter()
+    sel = O.select_head(q, k, w.block_size, density, 1.0, O.SORT_QK, O.COMP_DIAG)
+    t_sel = time.perf_counter() - t0
+    Qs = O.apply_permutation(q, sel.perm_q)
+    Ks = O.apply_permutation(k, sel.perm_k)
+    Vs = O.apply_permutation(v, sel.perm_k)
+    nq = sel.kv_index.shape[0]
+    rng = np.random.default_rng(seed)
+    blocks = sorted(set([0, nq - 1] + list(rng.choice(nq, size=min(nq, n_blocks), replace=False))))[:n_blocks]
+    t1 = time.perf_counter()
+    O.block_sparse_attention_head(Qs, Ks, Vs, sel.kv_index, w.block_size, 1.0 / math.sqrt(w.head_dim), blocks)
+    t_attn = time.perf_counter() - t1
+    # FLOPs of the sampled query blocks (ragged exact)
+    L = q.shape[0]
+    fl = 0
+    for g in blocks:
+        nqr = min(w.block_size, L - g * w.block_size)
+        for j in sel.kv_index[g]:
+            nkr = min(w.block_size, k.shape[0] - int(j) * w.block_size)
+            fl += 4 * nqr * nkr * w.head_dim
+    # selection pro-rated to the sampled share of the head's query blocks
+    secs = t_attn + t_sel * len(blocks) / nq
+    desc = (f"oracle (fp64 NumPy) on 1 q-head of the workload: full selection ({t_sel:.2f}s, pro-rated "
+            f"{len(blocks)}/{nq}) + block-sparse attention of {len(blocks)} query blocks ({t_attn:.2f}s)")
+    return fl, secs, desc
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # under torchrun only rank 0 runs the CPU oracle arm
+    from synth import CONFIGS, make_qkv
+    w = CONFIGS[args.config]
+    density = args.density if args.density is not None else w.density
+    # one head of the workload, generated on the host (same recipe as the GPU arm)
+    q, k, v = make_qkv(w, device="cpu", heads_q=1, heads_kv=1)
+    qn, kn, vn = q[0, 0].float().numpy(), k[0, 0].float().numpy(), v[0, 0].float().numpy()
+    n_blocks = 8 if w.seq_len >= 65536 else 16
+    for _ in range(args.warmup):
+        oracle_sample(w, qn, kn, vn, density, 2)
+    tot_fl, tot_s, desc = 0, 0.0, ""
+    for s in range(args.steps):
+        fl, secs, desc = oracle_sample(w, qn, kn, vn, density, n_blocks, seed=s)
+        tot_fl += fl
+        tot_s += secs
+    value = tot_fl / tot_s / 1e12
+    cores = cpu_cores()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": workload_desc(w, density), "seq_len": w.seq_len},
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from synth import CONFIGS, make_qkv
+    import paper_2605_19726_b200.baatt as ba
+    from paper_2605_19726_b200.dist import max_over_ranks, sum_over_ranks
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ba.load()
+    w = CONFIGS[args.config]
+    density = args.density if args.density is not None else w.density
+    # weak scaling: rank r processes batch element r (its own seeded inputs)
+    wr = w.with_(config_index=w.config_index + 100 * rank)
+    q, k, v = make_qkv(wr, device=dev)
+    torch.cuda.synchronize()
+    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag")
+    out = torch.empty_like(q)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ctx.select(q, k, v)
+        n_sel = ba.last_launch_count()
+        ctx.sparse_attn(out)
+        return n_sel + ba.last_launch_count()
+
+    for _ in range(max(args.warmup, 1)):
+        launches = step()
+    torch.cuda.synchronize()
+    flops_per_step = sparse_flops_from_index(ctx.sel.kv_index, ctx.sel.kv_count, q.shape[2], k.shape[2],
+                                             w.block_size, w.head_dim)
+    sampler = ClockSampler(local) if not args.profile else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        ctx.select(q, k, v)
+        ev[i][1].record(stream)
+        ctx.sparse_attn(out)
+        ev[i][2].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    total_ms = t_start.elapsed_time(t_end)
+    sel_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
+    attn_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+    ms_per_step = max_over_ranks(total_ms / args.steps, dev)
+    flops_all = sum_over_ranks(flops_per_step, dev)
+    value = flops_all / (ms_per_step * 1e-3) / 1e12
+    peaks = load_peaks()
+    attn_tflops = flops_per_step / (attn_ms * 1e-3) / 1e12
+
+    res = {}
+    if not args.no_dense and not args.profile:
+        # dense references on the same inputs: our tcgen05 kernel with every block
+        # (the 1/rho ceiling) and torch SDPA (cuDNN / flash) as an external check
+        dn_out = torch.empty_like(q)
+        for _ in range(2):
+            ba.ba_dense_attn(q, k, v, out=dn_out)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nrep = 3
+        e0.record(stream)
+        for _ in range(nrep):
+            ba.ba_dense_attn(q, k, v, out=dn_out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dense_ms = e0.elapsed_time(e1) / nrep
+        dense_flops = 4.0 * q.shape[0] * q.shape[1] * q.shape[2] * k.shape[2] * q.shape[3]
+        res["dense_ms"] = dense_ms
+        res["dense_tflops"] = dense_flops / (dense_ms * 1e-3) / 1e12
+        res["speedup_vs_dense"] = dense_ms / (total_ms / args.steps)
+        try:
+            import torch.nn.functional as F
+            for _ in range(2):
+                F.scaled_dot_product_attention(q, k, v, enable_gqa=q.shape[1] != k.shape[1])
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(nrep):
+                F.scaled_dot_product_attention(q, k, v, enable_gqa=q.shape[1] != k.shape[1])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            res["sdpa_ms"] = e0.elapsed_time(e1) / nrep
+            res["sdpa_tflops"] = dense_flops / (res["sdpa_ms"] * 1e-3) / 1e12
+            res["speedup_vs_sdpa"] = res["sdpa_ms"] / (total_ms / args.steps)
+        except Exception as ex:  # SDPA is context only
+            res["sdpa_error"] = str(ex)[:120]
+        del dn_out
+
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        qh, kh, vh = q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()
+        oh = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+        ws = torch.empty(ba.attention_host_workspace_size(qh, kh, vh, w.block_size, density), dtype=torch.uint8,
+                         device=dev)
+        ba.ba_attention_host(qh, kh, vh, oh, ws, w.block_size, density)
+        torch.cuda.synchronize()
+        n_e2e = max(2, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n_e2e):
+            ba.ba_attention_host(qh, kh, vh, oh, ws, w.block_size, density)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / n_e2e, dev)
+        h2d = (qh.numel() + kh.numel() + vh.numel()) * qh.element_size()
+        d2h = oh.numel() * oh.element_size()
+        e2e = {"value": flops_all / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "ba_attention_host (pinned host q/k/v -> H2D -> select + sparse attn -> D2H out)"}
+        del ws, qh, kh, vh, oh
+
+    cpu = None
+    if rank == 0 and not args.no_cpu and not args.profile and world == 1:
+        hsel = 0
+        qn = q[0, hsel].float().cpu().numpy()
+        kn = k[0, hsel * k.shape[1] // q.shape[1]].float().cpu().numpy()
+        vn = v[0, hsel * k.shape[1] // q.shape[1]].float().cpu().numpy()
+        n_blocks = 8 if w.seq_len >= 65536 else 16
+        fl, secs, desc = oracle_sample(w, qn, kn, vn, density, n_blocks)
+        cpu = {"value": fl / secs / 1e12, "unit": "TFLOP/s", "cores": cpu_cores(), "kind": "oracle", "sample": desc}
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tj = json.load(f)
+            if tj.get("config") == args.config:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        tokens = q.shape[2] * world
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": workload_desc(w, density), "global_batch": world, "seq_len": w.seq_len,
+                       "parallelism": f"batch-parallel x{world} (weak scaling, no data-path collective)",
+                       "l2": "inputs larger than L2 (q+k+v = %.2f GB per step)" %
+                             ((q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
+            "roofline": {"bound": "tensor", "kernel": "attn_sm100_tcgen05", "achieved": attn_tflops,
+                         "peak": peaks["tflops_sustained"], "unit": "TFLOP/s",
+                         "frac": attn_tflops / peaks["tflops_sustained"],
+                         "peak_kind": f"{peaks['source']} bf16 sustained (kernel timed inside a long step)",
+                         "frac_of_burst": attn_tflops / peaks["tflops_burst"],
+                         "flops_per_launch": flops_per_step, "ms_per_launch": attn_ms, "traffic": traffic},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "clocks": clocks,
+            "select_ms": sel_ms, "attn_ms": attn_ms, "select_share": sel_ms / (sel_ms + attn_ms),
+            "tokens_per_s": tokens / (ms_per_step * 1e-3),
+            "flops_per_step_per_rank": flops_per_step,
+        }
+        line.update(res)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

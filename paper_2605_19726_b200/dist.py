@@ -1,0 +1,72 @@
+"""Multi-GPU plumbing for the BA-Att hot path (one process per GPU).
+
+Every (batch, head) problem is independent (Alg. 1 is per head, PAPER.md
+P:527-569), so the path shards with no data-path collective:
+
+  * weak scaling (default, bench.py): rank r processes its own batch element;
+    nothing crosses NVLink.
+  * head-parallel (north star's 1/2/4/8-GPU split): rank r owns a contiguous
+    range of KV heads — whole GQA groups, so K/V never need replicating — and
+    the q-heads that read them; the only collective is one all-gather of O
+    along the head dimension to reassemble the output (NCCL over NVLink /
+    NVSwitch; gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+from typing import Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def head_range(heads_q: int, heads_kv: int, world: int, rank: int) -> Tuple[int, int, int, int]:
+    """(q0, q1, kv0, kv1): the q-head and kv-head ranges owned by `rank`.
+    KV heads are split as evenly as possible; q-heads follow their group."""
+    if heads_q % heads_kv:
+        raise ValueError("heads_q must be a multiple of heads_kv")
+    grp = heads_q // heads_kv
+    base, extra = divmod(heads_kv, world)
+    kv0 = rank * base + min(rank, extra)
+    kv1 = kv0 + base + (1 if rank < extra else 0)
+    return kv0 * grp, kv1 * grp, kv0, kv1
+
+
+def even_split(heads_q: int, heads_kv: int, world: int) -> bool:
+    return heads_kv % world == 0
+
+
+def gather_heads(out_local: torch.Tensor, heads_q: int, group=None) -> torch.Tensor:
+    """Reassemble O [b, Hq, L, d] from per-rank head slices [b, Hq_r, L, d].
+    Uses one all_gather_into_tensor when every rank holds the same number of
+    heads (the only collective of the path), else all_gather of padded slices."""
+    world = dist.get_world_size(group)
+    b, hr, L, d = out_local.shape
+    if hr * world == heads_q:
+        # gather along a leading dim, then move heads into place
+        flat = out_local.transpose(0, 1).contiguous()  # [hr, b, L, d]
+        full = torch.empty((world * hr, b, L, d), dtype=out_local.dtype, device=out_local.device)
+        dist.all_gather_into_tensor(full, flat, group=group)
+        return full.transpose(0, 1).contiguous()
+    counts = [None] * world
+    dist.all_gather_object(counts, hr, group=group)
+    hmax = max(counts)
+    pad = torch.zeros((hmax, b, L, d), dtype=out_local.dtype, device=out_local.device)
+    pad[:hr] = out_local.transpose(0, 1)
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    parts = [bufs[r][:counts[r]] for r in range(world)]
+    return torch.cat(parts, dim=0).transpose(0, 1).contiguous()
+
+
+def max_over_ranks(x: float, device) -> float:
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, device) -> float:
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
