@@ -7,22 +7,28 @@
 // renormalised over that support, then rows are written to the original
 // positions pi_q(i).  Non-causal.
 //
-// One CTA per query block (B = 128 rows, d = 128), 6 warps:
-//   warp 0  TMA producer: Q once, then K_j / V_j of the j-th selected block
-//           (index list kv_index) into a 2-stage ring each (128B swizzle).
-//   warp 1  MMA issuer (one thread): S_j = Q K_j^T into a double-buffered
-//           TMEM accumulator (SS form), then O += P_j V_j with P_j read from
-//           TMEM (TS form) — so the next S overlaps this tile's softmax.
-//   warps 2-5  softmax: one thread per query row; S_j TMEM -> registers,
-//           online softmax in the exp2 domain with lazy O rescaling (only
-//           when the running max grows by > 8, i.e. 2^8), P_j (bf16) written
-//           back into the S_j columns of TMEM; epilogue O / l -> bf16 rows at
-//           pi_q(i), plus optional LSE.
-// TMEM: S0 cols [0,128), S1 cols [128,256), O cols [256,384) (512 allocated).
+// One CTA per query block (B = 128 rows, d = 128), 11 warps:
+//   warps 0,10 TMA producers: K_j (warp 0) and V_j (warp 10) of the j-th
+//              selected key block (index list kv_index) into independent
+//              4-stage (K) and 2-stage (V) rings (128-byte swizzle).
+//   warp 1     MMA issuer (one thread) and TMEM owner.  S_j = Q K_j^T with Q
+//              held in TMEM (TS form: smem carries only K and V), into a
+//              double-buffered TMEM accumulator, then O += P_j V_j with P_j
+//              read from TMEM — S_{j+1} overlaps the softmax of tile j.
+//   warps 2-9  two softmax warpgroups; warpgroup h owns columns [64h, 64h+64)
+//              of every row (one thread per row and half), so each SMSP runs
+//              two softmax warps.  The halves swap partial row maxima once per
+//              tile through smem + a 64-thread named barrier; online softmax
+//              in the exp2 domain (FFMA2 / FMNMX3 / FADD2, part of the exp2 on
+//              the FMA pipe), lazy O rescaling (only when the running max grows
+//              by > 2^8), P_j (bf16) written back over S_j in TMEM; epilogue
+//              O / l -> bf16 rows at pi_q(i), plus optional LSE.
+// TMEM columns: S0 [0,128), S1 [128,256), O [256,384), Q [384,448).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -33,14 +39,18 @@ namespace sm100 {
 constexpr int BM = 128;          // query rows per tile (= block size B)
 constexpr int BN = 128;          // key rows per tile
 constexpr int HD = 128;          // head dim
-constexpr int NKS = 2;           // K stages
-constexpr int NVS = 2;           // V stages
+constexpr int NKS = 4;           // K stages
+constexpr int NVS = 2;           // V stages (V is consumed a tile after K)
 constexpr uint32_t BOX_BYTES = 128 * 64 * 2;     // one 128-row x 64-col bf16 box (16 KB)
 constexpr uint32_t TILE_BYTES = 2 * BOX_BYTES;   // 128 x 128 bf16 (32 KB)
 BA_DEVICE constexpr uint32_t s_col(int buf) { return buf ? 128u : 0u; }
 constexpr uint32_t O_COL = 256;
-constexpr int kThreads = 192;
+constexpr uint32_t Q_COL = 384;
+constexpr int kSoftmaxWarp0 = 2;
+constexpr int kVProducerWarp = 10;
+constexpr int kThreads = 352;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kDefaultEmu = 0;             // pairs per 8 on the polynomial exp2
 
 struct __align__(8) Bars {
   uint64_t q_full;
@@ -51,11 +61,12 @@ struct __align__(8) Bars {
   uint32_t tmem_base;
 };
 
-constexpr uint32_t SMEM_Q = 0;
-constexpr uint32_t SMEM_K = TILE_BYTES;
+constexpr uint32_t SMEM_K = 0;
 constexpr uint32_t SMEM_V = SMEM_K + NKS * TILE_BYTES;
-constexpr uint32_t SMEM_BARS = SMEM_V + NVS * TILE_BYTES;
-constexpr uint32_t SMEM_BYTES = SMEM_BARS + 256 + 1024;  // + alignment slack
+constexpr uint32_t SMEM_RED = SMEM_V + NVS * TILE_BYTES;       // float [2][2][128] row-max exchange
+constexpr uint32_t SMEM_RED2 = SMEM_RED + 2 * 2 * 128 * 4;     // float [2][128] final l exchange
+constexpr uint32_t SMEM_BARS = SMEM_RED2 + 2 * 128 * 4;
+constexpr uint32_t SMEM_BYTES = SMEM_BARS + 256 + 1024;       // + alignment slack
 
 // ------------------------------------------------------------------ PTX wrappers
 BA_DEVICE uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -85,6 +96,7 @@ BA_DEVICE void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sy
 BA_DEVICE void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 BA_DEVICE void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 BA_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+BA_DEVICE void named_bar_sync(int id, int count) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory"); }
 
 BA_DEVICE void tma_prefetch(const CUtensorMap *m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
@@ -126,6 +138,50 @@ BA_DEVICE float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+BA_DEVICE float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// Packed fp32x2 ops (FFMA2 / FADD2 on sm_100): half the issue slots of scalar fp32.
+BA_DEVICE uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+BA_DEVICE void unf2(uint64_t v, float &lo, float &hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+BA_DEVICE uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+BA_DEVICE uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for a pair on the FMA/ALU pipes (offloads the MUFU, FA4-style):
+// x = xi + f with xi = rint(x) via the 1.5*2^23 trick, 2^f by a degree-3
+// minimax polynomial on [-1/2, 1/2] (max rel. error 2.3e-4, below bf16's
+// 2^-9), 2^xi added into the exponent bits.  Inputs are clamped to >= -126.
+BA_DEVICE uint64_t exp2_poly2(uint64_t x2) {
+  float x0, x1;
+  unf2(x2, x0, x1);
+  x2 = f2(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t magic = f2(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(x2, magic);
+  const uint64_t xi = fadd2(t, f2(-12582912.f, -12582912.f));
+  const uint64_t fr = ffma2(xi, f2(-1.f, -1.f), x2);
+  uint64_t p = ffma2(f2(0.0554986224f, 0.0554986224f), fr, f2(0.243548840f, 0.243548840f));
+  p = ffma2(p, fr, f2(0.693232119f, 0.693232119f));
+  p = ffma2(p, fr, f2(0.999772966f, 0.999772966f));
+  float p0, p1, t0, t1;
+  unf2(p, p0, p1);
+  unf2(t, t0, t1);
+  const float r0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  const float r1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+  return f2(r0, r1);
+}
 BA_DEVICE uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -151,18 +207,33 @@ constexpr uint32_t IDESC_BASE = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)
 constexpr uint32_t IDESC_S = IDESC_BASE;              // A K-major (Q), B K-major (K)
 constexpr uint32_t IDESC_O = IDESC_BASE | (1u << 16); // B MN-major (V: d contiguous)
 
+// kEmu: of every 8 element pairs of a row tile, how many take the polynomial
+// exp2 (FMA pipe) instead of MUFU.EX2.
+// kNoSoftmax: profiling-only variant (BA_ATTN_DEBUG=1) in which the softmax
+// warps hand S straight back without touching it — it measures the MMA + TMA
+// pipeline ceiling; its output is meaningless.
+// kTrace: profiling-only variant (BA_ATTN_TRACE=1): CTA (0,0) records clock64
+// timestamps of the first kTraceTiles tiles for the producer, MMA and one
+// softmax warp of each half, and prints them.
+constexpr int kTraceTiles = 12;
+template <int kEmu, bool kNoSoftmax = false, bool kTrace = false>
 __global__ void __launch_bounds__(kThreads, 1)
-attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                  const __grid_constant__ CUtensorMap tm_v) {
+attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t *smem = smem_raw + (base - raw);
   Bars &bars = *reinterpret_cast<Bars *>(smem + SMEM_BARS);
+  float *red = reinterpret_cast<float *>(smem + SMEM_RED);    // [2][2][128]
+  float *red2 = reinterpret_cast<float *>(smem + SMEM_RED2);  // [2][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = blockIdx.x;
   const int64_t bh = blockIdx.y;
+  __shared__ long long trace[16][kTraceTiles];
+  const bool tr = kTrace && blockIdx.x == 0 && blockIdx.y == 0;
+  const long long t_origin = kTrace ? clock64() : 0;
+#define TR(slot, j) do { if (tr && (j) < kTraceTiles) trace[slot][j] = clock64() - t_origin; } while (0)
   const int64_t b = bh / a.hq, h = bh - b * a.hq;
   const int64_t hk = h / (a.hq / a.hkv);
   const int64_t row = bh * a.nq + gq;
@@ -170,15 +241,14 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, co
   const int32_t *idx = a.kv_index ? a.kv_index + row * a.kv_stride : nullptr;
 
   if (warp == 0 && lane == 0) {
-    mbar_init(&bars.q_full, 1);
+    mbar_init(&bars.q_full, 8);   // one elected arrive per softmax warp
     for (int s = 0; s < NKS; ++s) { mbar_init(&bars.k_full[s], 1); mbar_init(&bars.k_empty[s], 1); }
     for (int s = 0; s < NVS; ++s) { mbar_init(&bars.v_full[s], 1); mbar_init(&bars.v_empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&bars.s_full[s], 1); mbar_init(&bars.p_full[s], 128); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&bars.s_full[s], 1); mbar_init(&bars.p_full[s], 8); }
     mbar_init(&bars.o_done, 1);
     fence_barrier_init();
-    tma_prefetch(&tm_q);
     tma_prefetch(&tm_k);
-    tma_prefetch(&tm_v);
+    tma_prefetch(&tm_v);  // (both producers read their own map)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&bars.tmem_base)), "r"(512));
@@ -189,53 +259,45 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, co
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
 
-  if (warp == 0) {
-    // ================================================================ TMA producer
+  if (warp == 0 || warp == kVProducerWarp) {
+    // ================================================================ TMA producers
+    // warp 0 streams K_j, the last warp streams V_j: independent rings, so a
+    // wait for a free V slot never delays the next K load (and vice versa).
+    const bool is_k = warp == 0;
+    const int nst = is_k ? NKS : NVS;
+    const CUtensorMap *map = is_k ? &tm_k : &tm_v;
+    uint64_t *full = is_k ? bars.k_full : bars.v_full;
+    uint64_t *empty = is_k ? bars.k_empty : bars.v_empty;
+    const uint32_t ring = base + (is_k ? SMEM_K : SMEM_V);
     if (lane == 0 && cnt > 0) {
-      const uint32_t sq = base + SMEM_Q;
-      mbar_expect_tx(&bars.q_full, TILE_BYTES);
-      tma_load_4d(sq, &tm_q, &bars.q_full, 0, gq * BM, (int)h, (int)b);
-      tma_load_4d(sq + BOX_BYTES, &tm_q, &bars.q_full, 64, gq * BM, (int)h, (int)b);
-      for (int j = 0; j <= cnt; ++j) {
-        if (j < cnt) {
-          const int s = j % NKS;
-          const uint32_t ph = (uint32_t)(j / NKS) & 1u;
-          mbar_wait(&bars.k_empty[s], ph ^ 1u);
-          const int gk = idx ? idx[j] : j;
-          const uint32_t dst = base + SMEM_K + s * TILE_BYTES;
-          mbar_expect_tx(&bars.k_full[s], TILE_BYTES);
-          tma_load_4d(dst, &tm_k, &bars.k_full[s], 0, gk * BN, (int)hk, (int)b);
-          tma_load_4d(dst + BOX_BYTES, &tm_k, &bars.k_full[s], 64, gk * BN, (int)hk, (int)b);
-        }
-        if (j >= 1) {
-          const int jv = j - 1;
-          const int s = jv % NVS;
-          const uint32_t ph = (uint32_t)(jv / NVS) & 1u;
-          mbar_wait(&bars.v_empty[s], ph ^ 1u);
-          const int gk = idx ? idx[jv] : jv;
-          const uint32_t dst = base + SMEM_V + s * TILE_BYTES;
-          mbar_expect_tx(&bars.v_full[s], TILE_BYTES);
-          tma_load_4d(dst, &tm_v, &bars.v_full[s], 0, gk * BN, (int)hk, (int)b);
-          tma_load_4d(dst + BOX_BYTES, &tm_v, &bars.v_full[s], 64, gk * BN, (int)hk, (int)b);
-        }
+      for (int j = 0; j < cnt; ++j) {
+        const int s = j % nst;
+        const uint32_t ph = (uint32_t)(j / nst) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        TR(is_k ? 0 : 1, j);
+        const int gk = idx ? idx[j] : j;
+        const uint32_t dst = ring + s * TILE_BYTES;
+        mbar_expect_tx(&full[s], TILE_BYTES);
+        tma_load_4d(dst, map, &full[s], 0, gk * BN, (int)hk, (int)b);
+        tma_load_4d(dst + BOX_BYTES, map, &full[s], 64, gk * BN, (int)hk, (int)b);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     // ================================================================ MMA issuer
     if (lane == 0 && cnt > 0) {
-      const uint32_t sq = base + SMEM_Q;
       mbar_wait(&bars.q_full, 0);
+      tc_fence_after();
       auto issue_s = [&](int j) {
         const int s = j % NKS;
         mbar_wait(&bars.k_full[s], (uint32_t)(j / NKS) & 1u);
+        TR(2, j);
         tc_fence_after();
         const uint32_t sk = base + SMEM_K + s * TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * BOX_BYTES + (kk & 3) * 32;
-          mma_ss(tmem + s_col(j & 1), make_desc(sq + off, 16, 1024), make_desc(sk + off, 16, 1024), IDESC_S,
-                 kk > 0 ? 1u : 0u);
+          mma_ts(tmem + s_col(j & 1), tmem + Q_COL + kk * 8, make_desc(sk + off, 16, 1024), IDESC_S, kk > 0 ? 1u : 0u);
         }
         mma_commit(&bars.k_empty[s]);
         mma_commit(&bars.s_full[j & 1]);
@@ -244,8 +306,10 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, co
       for (int j = 0; j < cnt; ++j) {
         if (j + 1 < cnt) issue_s(j + 1);
         mbar_wait(&bars.p_full[j & 1], (uint32_t)(j >> 1) & 1u);
+        TR(3, j);
         const int s = j % NVS;
         mbar_wait(&bars.v_full[s], (uint32_t)(j / NVS) & 1u);
+        TR(4, j);
         tc_fence_after();
         const uint32_t sv = base + SMEM_V + s * TILE_BYTES;
 #pragma unroll
@@ -258,98 +322,168 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, co
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp >= kSoftmaxWarp0 && warp < kSoftmaxWarp0 + 8) {
     // ================================================================ softmax + epilogue
-    const int qd = warp & 3;             // TMEM lane quadrant of this warp
-    const int r = qd * 32 + lane;        // query row within the tile
+    const int sw = warp - kSoftmaxWarp0;  // 0..7
+    const int hf = sw >> 2;               // column half owned by this warpgroup
+    const int qd = warp & 3;              // TMEM lane quadrant of this warp
+    const int r = qd * 32 + lane;         // query row within the tile
     const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
+    const int64_t row0 = (int64_t)gq * BM;
+    const int nrows = (int)imin64(BM, a.lq - row0);
+    // Q row half -> TMEM (A operand of S = Q K^T): element pairs packed per column
+    {
+      uint32_t qv[32];
+      const __nv_bfloat16 *qp = static_cast<const __nv_bfloat16 *>(a.q) + b * a.qs[0] + h * a.qs[1] +
+                                (row0 + r) * a.qs[2] + hf * 64;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 u = r < nrows ? ldg16(qp + 8 * i) : make_uint4(0, 0, 0, 0);
+        qv[4 * i] = u.x; qv[4 * i + 1] = u.y; qv[4 * i + 2] = u.z; qv[4 * i + 3] = u.w;
+      }
+      tmem_st_x32(trow + Q_COL + hf * 32, qv);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.q_full);
+    }
     const float c = a.scale * 1.4426950408889634f;  // scale * log2(e)
     const int64_t ragged_valid = a.lk - (a.nk - 1) * (int64_t)BN;  // rows in the last key block
+    const bool ragged = ragged_valid < BN;
     float m = -INFINITY, l = 0.f;
-    uint32_t sr[128];
+    uint32_t sr[64];
     for (int j = 0; j < cnt; ++j) {
       mbar_wait(&bars.s_full[j & 1], (uint32_t)(j >> 1) & 1u);
+      if (lane == 0 && qd == 0) TR(5 + 5 * hf, j);
       tc_fence_after();
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) tmem_ld_x32(trow + s_col(j & 1) + q4 * 32, sr + q4 * 32);
-      tmem_wait_ld();
-      const int gk = idx ? idx[j] : j;
-      if (gk == a.nk - 1 && ragged_valid < BN) {
-#pragma unroll
-        for (int i = 0; i < 128; ++i)
-          if (i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
+      if constexpr (kNoSoftmax) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.p_full[j & 1]);
+        continue;
       }
-      float mx = -INFINITY;
+      tmem_ld_x32(trow + s_col(j & 1) + hf * 64, sr);
+      tmem_ld_x32(trow + s_col(j & 1) + hf * 64 + 32, sr + 32);
+      tmem_wait_ld();
+      if (lane == 0 && qd == 0) TR(6 + 5 * hf, j);
+      if (ragged) {
+        const int gk = idx ? idx[j] : j;
+        if (gk == a.nk - 1) {
 #pragma unroll
-      for (int i = 0; i < 128; ++i) mx = fmaxf(mx, __uint_as_float(sr[i]));
-      const float mt = mx * c;
-      float corr = 1.f;
+          for (int i = 0; i < 64; ++i)
+            if (hf * 64 + i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
+        }
+      }
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 64; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          m4[u] = fmax3(m4[u], __uint_as_float(sr[i + 2 * u]), __uint_as_float(sr[i + 2 * u + 1]));
+      }
+      const float pmax = fmaxf(fmax3(m4[0], m4[1], m4[2]), m4[3]);
+      // swap partial maxima with the other half of the row (red is double-buffered by j)
+      red[((j & 1) * 2 + hf) * 128 + r] = pmax;
+      tc_fence_before();
+      named_bar_sync(1 + qd, 64);
+      tc_fence_after();
+      if (lane == 0 && qd == 0) TR(7 + 5 * hf, j);
+      const float mt = fmaxf(pmax, red[((j & 1) * 2 + (hf ^ 1)) * 128 + r]) * c;
       if (j == 0) {
         m = mt;
       } else {
         const bool need = mt > m + kRescaleThreshold;
-        if (__any_sync(0xffffffffu, need)) {
+        if (__any_sync(0xffffffffu, need)) {  // same rows -> same decision in both halves
+          float corr = 1.f;
           if (need) { corr = ex2(m - mt); m = mt; }
           mbar_wait(&bars.o_done, (uint32_t)(j - 1) & 1u);
           tc_fence_after();
           uint32_t ov[32];
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            tmem_ld_x32(trow + O_COL + q4 * 32, ov);
+          for (int q2 = 0; q2 < 2; ++q2) {
+            tmem_ld_x32(trow + O_COL + hf * 64 + q2 * 32, ov);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
-            tmem_st_x32(trow + O_COL + q4 * 32, ov);
+            tmem_st_x32(trow + O_COL + hf * 64 + q2 * 32, ov);
           }
           l *= corr;
         }
       }
-      float sum = 0.f;
-      const float negm = -m;
+      // p = 2^(s*c - m): FFMA2 for the argument, MUFU or polynomial exp2, FADD2 row sums
+      const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
+      uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-      for (int i = 0; i < 128; i += 2) {
-        const float p0 = ex2(fmaf(__uint_as_float(sr[i]), c, negm));
-        const float p1 = ex2(fmaf(__uint_as_float(sr[i + 1]), c, negm));
-        sum += p0 + p1;
-        sr[i >> 1] = pack_bf16(p0, p1);
+      for (int i = 0; i < 32; ++i) {
+        const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
+        uint64_t p2;
+        if ((i & 7) < kEmu) {
+          p2 = exp2_poly2(x2);
+        } else {
+          float x0, x1;
+          unf2(x2, x0, x1);
+          p2 = f2(ex2(x0), ex2(x1));
+        }
+        acc2[i & 3] = fadd2(acc2[i & 3], p2);
+        float p0, p1;
+        unf2(p2, p0, p1);
+        sr[i] = pack_bf16(p0, p1);
       }
-      l += sum;
-      tmem_st_x32(trow + s_col(j & 1), sr);
-      tmem_st_x32(trow + s_col(j & 1) + 32, sr + 32);
+      {
+        const uint64_t t2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
+        float a0, a1;
+        unf2(t2, a0, a1);
+        l += a0 + a1;
+      }
+      if (lane == 0 && qd == 0) TR(8 + 5 * hf, j);
+      tmem_st_x32(trow + s_col(j & 1) + hf * 32, sr);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&bars.p_full[j & 1]);
+      __syncwarp();  // all 32 lanes' P stores are complete before the warp's single arrive
+      if (lane == 0) mbar_arrive(&bars.p_full[j & 1]);
+      if (lane == 0 && qd == 0) TR(9 + 5 * hf, j);
     }
-    // epilogue
-    const int64_t row0 = (int64_t)gq * BM;
-    const int nrows = (int)imin64(BM, a.lq - row0);
+    // epilogue: l = sum of both halves; each half writes its 64 output columns
+    red2[hf * 128 + r] = l;
+    named_bar_sync(1 + qd, 64);
+    const float lt = l + red2[(hf ^ 1) * 128 + r];
     if (cnt > 0) {
       mbar_wait(&bars.o_done, (uint32_t)(cnt - 1) & 1u);
       tc_fence_after();
     }
-    const float inv = cnt > 0 ? 1.f / l : 0.f;
+    const float inv = cnt > 0 ? 1.f / lt : 0.f;
     int64_t orow = row0 + r;
     if (r < nrows && a.perm_q) orow = a.perm_q[bh * a.lq + row0 + r];
-    __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(a.out) + b * a.os[0] + h * a.os[1] + orow * a.os[2];
+    __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(a.out) + b * a.os[0] + h * a.os[1] + orow * a.os[2] + hf * 64;
 #pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4) {
+    for (int q2 = 0; q2 < 2; ++q2) {
       uint32_t ov[32];
-      tmem_ld_x32(trow + O_COL + q4 * 32, ov);
+      tmem_ld_x32(trow + O_COL + hf * 64 + q2 * 32, ov);
       tmem_wait_ld();
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i)
         pk[i] = pack_bf16(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
       if (r < nrows) {
-        uint4 *dst = reinterpret_cast<uint4 *>(o + q4 * 32);
+        uint4 *dst = reinterpret_cast<uint4 *>(o + q2 * 32);
 #pragma unroll
         for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
       }
     }
-    if (a.lse && r < nrows) a.lse[bh * a.lq + orow] = cnt > 0 ? (m + log2f(l)) * 0.69314718055994531f : -INFINITY;
+    if (a.lse && hf == 0 && r < nrows) a.lse[bh * a.lq + orow] = cnt > 0 ? (m + log2f(lt)) * 0.69314718055994531f : -INFINITY;
   }
   tc_fence_before();
   __syncthreads();
+  if (tr && threadIdx.x == 0) {
+    const char *names[15] = {"prod_K", "prod_V", "mma_S", "mma_pwait", "mma_PV", "s0_wait", "s0_ld", "s0_bar",
+                             "s0_exp", "s0_arr", "s1_wait", "s1_ld", "s1_bar", "s1_exp", "s1_arr"};
+    for (int k = 0; k < 15; ++k) {
+      printf("TRACE %-9s", names[k]);
+      for (int j = 0; j < kTraceTiles && j < cnt; ++j) printf(" %7lld", trace[k][j]);
+      printf("\n");
+    }
+  }
+#undef TR
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -392,19 +526,57 @@ bool attn_sm100_supported(const AttnArgs &a) { return a.dtype == 0 && a.d == 128
 
 cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
   using namespace sm100;
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mk, mv;
   if (!get_encode()) return cudaErrorNotSupported;  // no TMA encoder: fail loudly, never fall back
-  if (!make_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs) || !make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) ||
-      !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs))
+  if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) || !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs))
     return cudaErrorInvalidValue;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
+  // exp2 offload fraction: compile-time variants, BA_EXP_EMU=0..4 selects one (tuning knob)
+  static int emu = -1;
+  if (emu < 0) {
+    const char *env = getenv("BA_EXP_EMU");
+    emu = env ? atoi(env) : kDefaultEmu;
+    if (emu < 0 || emu > 4) emu = kDefaultEmu;
   }
   dim3 grid((unsigned)a.nq, (unsigned)(a.batch * a.hq));
-  attn_sm100_kernel<<<grid, kThreads, SMEM_BYTES, st>>>(a, mq, mk, mv);
+#define BA_LAUNCH(E)                                                                                          \
+  do {                                                                                                        \
+    static bool attr = false;                                                                                 \
+    if (!attr) {                                                                                              \
+      cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           (int)SMEM_BYTES);                                                  \
+      if (e != cudaSuccess) return e;                                                                         \
+      attr = true;                                                                                            \
+    }                                                                                                         \
+    attn_sm100_kernel<E><<<grid, kThreads, SMEM_BYTES, st>>>(a, mk, mv);                                  \
+  } while (0)
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char *env = getenv("BA_ATTN_DEBUG");
+    dbg = env ? atoi(env) : 0;
+  }
+  if (dbg == 2) {
+    cudaFuncSetAttribute(attn_sm100_kernel<kDefaultEmu, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    attn_sm100_kernel<kDefaultEmu, false, true><<<grid, kThreads, SMEM_BYTES, st>>>(a, mk, mv);
+    return cudaGetLastError();
+  }
+  if (dbg == 3) {
+    cudaFuncSetAttribute(attn_sm100_kernel<0, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    attn_sm100_kernel<0, true, true><<<grid, kThreads, SMEM_BYTES, st>>>(a, mk, mv);
+    return cudaGetLastError();
+  }
+  if (dbg == 1) {
+    cudaFuncSetAttribute(attn_sm100_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    attn_sm100_kernel<0, true><<<grid, kThreads, SMEM_BYTES, st>>>(a, mk, mv);
+    return cudaGetLastError();
+  }
+  switch (emu) {
+    case 0: BA_LAUNCH(0); break;
+    case 1: BA_LAUNCH(1); break;
+    case 2: BA_LAUNCH(2); break;
+    case 4: BA_LAUNCH(4); break;
+    default: BA_LAUNCH(3); break;
+  }
+#undef BA_LAUNCH
   return cudaGetLastError();
 }
 
