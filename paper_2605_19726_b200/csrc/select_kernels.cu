@@ -37,51 +37,71 @@ namespace baatt {
 // partial sums are combined with xor offsets 8, 4, 2, 1 (a+b == b+a exactly,
 // so every lane of a pair holds the oracle's p[l] + p[l+8], ...).
 // =====================================================================================
+constexpr int kNormRows = 4;  // rows per half-warp: 4 independent 16-byte loads in flight per lane
+
 template <typename T, int D>
 __global__ void __launch_bounds__(256) norm_keys_kernel(const T *__restrict__ x, int64_t s0, int64_t s1,
                                                         int64_t s2, int64_t heads, int64_t L,
                                                         float *__restrict__ keys,
                                                         float *__restrict__ keys_user) {
   constexpr int PER_LANE = D / 16;  // 4 or 8 elements
+  constexpr int BYTES = PER_LANE * (int)sizeof(T);
   const int lane16 = threadIdx.x & 15;
-  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 4;
-  const int64_t total = int64_t(gridDim.y) * heads * L;  // gridDim.y = batch
-  (void)total;
+  const int64_t hw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 4;  // half-warp id
   const int64_t bh_rows = heads * L;
   const int64_t b = blockIdx.y;
-  if (row >= bh_rows) return;  // whole half-warps exit together
-  const int64_t h = row / L, t = row - h * L;
-  const T *p = x + b * s0 + h * s1 + t * s2 + lane16 * PER_LANE;
-  float f[PER_LANE];
-  if constexpr (sizeof(T) * PER_LANE == 16) {
-    uint4 u = ldg16(p);
-    Chunk<T>::unpack(u, *reinterpret_cast<float(*)[16 / sizeof(T)]>(f));
-  } else if constexpr (sizeof(T) * PER_LANE == 32) {
-    float a[4], c[4];
-    Chunk<T>::unpack(ldg16(p), a);
-    Chunk<T>::unpack(ldg16(p + 4), c);
+  uint4 raw[kNormRows][BYTES > 16 ? 2 : 1];
+  int64_t rows[kNormRows];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) { f[i] = a[i]; f[4 + i] = c[i]; }
-  } else {  // bf16, d = 64: 8 bytes
-    uint2 u = __ldg(reinterpret_cast<const uint2 *>(p));
-    f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xffff0000u);
-    f[2] = __uint_as_float(u.y << 16); f[3] = __uint_as_float(u.y & 0xffff0000u);
+  for (int k = 0; k < kNormRows; ++k) {  // issue every load first
+    const int64_t row = hw * kNormRows + k;
+    rows[k] = row;
+    if (row < bh_rows) {
+      const int64_t h = row / L, t = row - h * L;
+      const T *p = x + b * s0 + h * s1 + t * s2 + lane16 * PER_LANE;
+      if constexpr (BYTES == 8) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2 *>(p));
+        raw[k][0] = make_uint4(u.x, u.y, 0, 0);
+      } else {
+        raw[k][0] = ldg16(p);
+        if constexpr (BYTES > 16) raw[k][BYTES > 16 ? 1 : 0] = ldg16(p + 16 / sizeof(T));
+      }
+    }
   }
-  double s = 0.0;
 #pragma unroll
-  for (int i = 0; i < PER_LANE; ++i) {
-    const double v = static_cast<double>(f[i]);
-    s = fma(v, v, s);  // v*v is exact in fp64, so fma == mul-then-add
-  }
-  s += __shfl_xor_sync(0xffffffffu, s, 8);
-  s += __shfl_xor_sync(0xffffffffu, s, 4);
-  s += __shfl_xor_sync(0xffffffffu, s, 2);
-  s += __shfl_xor_sync(0xffffffffu, s, 1);
-  if (lane16 == 0) {
-    const float k = __double2float_rn(s);
-    const int64_t o = b * bh_rows + row;
-    keys[o] = k;
-    if (keys_user) keys_user[o] = k;
+  for (int k = 0; k < kNormRows; ++k) {
+    float f[PER_LANE];
+    if constexpr (sizeof(T) == 2) {
+      const uint32_t w[4] = {raw[k][0].x, raw[k][0].y, raw[k][0].z, raw[k][0].w};
+#pragma unroll
+      for (int i = 0; i < PER_LANE / 2; ++i) {
+        f[2 * i] = __uint_as_float(w[i] << 16);
+        f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < PER_LANE; ++i) {
+        const uint4 &u = raw[k][i / 4];
+        const uint32_t w = (i & 3) == 0 ? u.x : (i & 3) == 1 ? u.y : (i & 3) == 2 ? u.z : u.w;
+        f[i] = __uint_as_float(w);
+      }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < PER_LANE; ++i) {
+      const double v = static_cast<double>(f[i]);
+      s = fma(v, v, s);  // v*v is exact in fp64, so fma == mul-then-add
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 8);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (lane16 == 0 && rows[k] < bh_rows) {
+      const float key = __double2float_rn(s);
+      const int64_t o = b * bh_rows + rows[k];
+      keys[o] = key;
+      if (keys_user) keys_user[o] = key;
+    }
   }
 }
 
@@ -89,7 +109,8 @@ cudaError_t launch_norm_keys(int dtype, int d, const void *x, const int64_t *st,
                              int64_t heads, int64_t L, float *keys, float *keys_user,
                              cudaStream_t stream) {
   const int64_t rows = heads * L;
-  dim3 grid((unsigned)((rows * 16 + 255) / 256), (unsigned)batch);
+  const int64_t halfwarps = (rows + kNormRows - 1) / kNormRows;
+  dim3 grid((unsigned)((halfwarps * 16 + 255) / 256), (unsigned)batch);
   if (dtype == 0 && d == 128)
     norm_keys_kernel<__nv_bfloat16, 128><<<grid, 256, 0, stream>>>((const __nv_bfloat16 *)x, st[0], st[1], st[2], heads, L, keys, keys_user);
   else if (dtype == 0 && d == 64)
@@ -308,7 +329,7 @@ cudaError_t launch_radix_sort(const SortGeom &g, uint32_t *keys_a, uint32_t *val
 // registers between the copy, the mean pass and the variance pass.
 // =====================================================================================
 template <typename T, int D>
-__global__ void __launch_bounds__(256) gather_stats_kernel(
+__global__ void __launch_bounds__(256, 3) gather_stats_kernel(
     const T *__restrict__ x, int64_t s0, int64_t s1, int64_t s2, int64_t heads, int64_t L, int B,
     const int32_t *__restrict__ perm, int32_t *__restrict__ perm_id_out, T *__restrict__ xs,
     double *__restrict__ mean, double *__restrict__ var) {
@@ -327,7 +348,26 @@ __global__ void __launch_bounds__(256) gather_stats_kernel(
   const int n = (int)imin64(B, L - row0);
   const T *xbase = x + b * s0 + h * s1 + chunk * EPC;
   T *xsbase = xs + (bh * L + row0) * D + chunk * EPC;
-  float vals[MAXIT][EPC];
+  // stage 1: source row indices; stage 2: every row load in flight; stage 3: stores + sums
+  int32_t src[MAXIT];  // L < 2^31 (validated)
+#pragma unroll
+  for (int it = 0; it < MAXIT; ++it) {
+    const int r = rsub + it * RPI;
+    src[it] = -1;
+    if (r < n) {
+      const int64_t tok = row0 + r;
+      if (perm) {
+        src[it] = __ldg(perm + bh * L + tok);
+      } else {
+        src[it] = (int32_t)tok;
+        if (perm_id_out && chunk == 0) perm_id_out[bh * L + tok] = (int32_t)tok;
+      }
+    }
+  }
+  uint4 raw[MAXIT];
+#pragma unroll
+  for (int it = 0; it < MAXIT; ++it)
+    raw[it] = src[it] >= 0 ? ldg16(xbase + (int64_t)src[it] * s2) : make_uint4(0, 0, 0, 0);
   double acc[EPC];
 #pragma unroll
   for (int e = 0; e < EPC; ++e) acc[e] = 0.0;
@@ -335,15 +375,11 @@ __global__ void __launch_bounds__(256) gather_stats_kernel(
   for (int it = 0; it < MAXIT; ++it) {
     const int r = rsub + it * RPI;
     if (r < n) {
-      const int64_t tok = row0 + r;
-      int64_t src = tok;
-      if (perm) src = __ldg(perm + bh * L + tok);
-      else if (perm_id_out && chunk == 0) perm_id_out[bh * L + tok] = (int32_t)tok;
-      const uint4 u = ldg16(xbase + src * s2);
-      stg16(xsbase + (int64_t)r * D, u);
-      Chunk<T>::unpack(u, vals[it]);
+      stg16(xsbase + (int64_t)r * D, raw[it]);
+      float v[EPC];
+      Chunk<T>::unpack(raw[it], v);
 #pragma unroll
-      for (int e = 0; e < EPC; ++e) acc[e] += (double)vals[it][e];
+      for (int e = 0; e < EPC; ++e) acc[e] += (double)v[e];
     }
   }
   if (!mean) return;  // V: copy only
@@ -364,9 +400,11 @@ __global__ void __launch_bounds__(256) gather_stats_kernel(
   for (int it = 0; it < MAXIT; ++it) {
     const int r = rsub + it * RPI;
     if (r < n) {
+      float v[EPC];
+      Chunk<T>::unpack(raw[it], v);
 #pragma unroll
       for (int e = 0; e < EPC; ++e) {
-        const double dv = (double)vals[it][e] - mu[e];
+        const double dv = (double)v[e] - mu[e];
         acc[e] = fma(dv, dv, acc[e]);
       }
     }
@@ -401,8 +439,8 @@ cudaError_t launch_gather_stats(int dtype, int d, const void *x, const int64_t *
 // =====================================================================================
 // K4a: compensated block logits as an fp64 micro-GEMM over 3d features.
 // =====================================================================================
-constexpr int kScTile = 64;
-constexpr int kScK = 16;
+constexpr int kScTile = 128;  // output tile 128 x 128, 256 threads, 8 x 8 per thread
+constexpr int kScK = 8;       // features per smem stage
 
 template <int D>
 __global__ void __launch_bounds__(256) scores_kernel(int64_t hq, int64_t grp, int64_t nq, int64_t nk,
@@ -412,8 +450,8 @@ __global__ void __launch_bounds__(256) scores_kernel(int64_t hq, int64_t grp, in
                                                      const double *__restrict__ k_var, int comp,
                                                      double inv_sqrt_d, double beta_over_d,
                                                      double *__restrict__ logits) {
-  __shared__ double As[kScK][kScTile + 2];
-  __shared__ double Bs[kScK][kScTile + 2];
+  __shared__ __align__(16) double As[2][kScK][kScTile + 2];
+  __shared__ __align__(16) double Bs[2][kScK][kScTile + 2];
   const int64_t bhq = blockIdx.z;            // batch * hq + head
   const int64_t b = bhq / hq, h = bhq - b * hq;
   const int64_t bhk = b * (hq / grp) + h / grp;
@@ -421,54 +459,65 @@ __global__ void __launch_bounds__(256) scores_kernel(int64_t hq, int64_t grp, in
   const double *qm = q_mean + bhq * nq * D, *qv = q_var + bhq * nq * D;
   const double *km = k_mean + bhk * nk * D, *kv = k_var + bhk * nk * D;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[4][4];
+  double acc[8][8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
   const int nfeat = comp ? 3 * D : D;
-  for (int c0 = 0; c0 < nfeat; c0 += kScK) {
-    // load 64 rows x 16 features of each side; thread -> (row = tid/4, 4 features)
-    {
-      const int r = threadIdx.x >> 2, f0 = (threadIdx.x & 3) * 4;
+  // loader: thread -> (row = tid / 2, 4 features); features of part p at column t:
+  //   Xq = [Qbar/sqrt(d), (beta/d) VarQ, (beta/d) Qbar^2],  Xk = [Kbar, Kbar^2 + VarK, VarK]
+  const int lr = threadIdx.x >> 1, lf = (threadIdx.x & 1) * 4;
+  auto load = [&](int c0, int buf) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int c = c0 + f0 + e;
-        const int part = c / D, t = c - part * D;
-        const int64_t gq = gq0 + r, gk = gk0 + r;
-        double a = 0.0, bb = 0.0;
-        if (gq < nq) {
-          const double m = qm[gq * D + t];
-          a = part == 0 ? m * inv_sqrt_d : part == 1 ? beta_over_d * qv[gq * D + t] : beta_over_d * (m * m);
-        }
-        if (gk < nk) {
-          const double m = km[gk * D + t];
-          bb = part == 0 ? m : part == 1 ? fma(m, m, kv[gk * D + t]) : kv[gk * D + t];
-        }
-        As[f0 + e][r] = a;
-        Bs[f0 + e][r] = bb;
+    for (int e = 0; e < 4; ++e) {
+      const int c = c0 + lf + e;
+      const int part = c / D, t = c - part * D;
+      const int64_t gq = gq0 + lr, gk = gk0 + lr;
+      double a = 0.0, bb = 0.0;
+      if (gq < nq) {
+        const double m = qm[gq * D + t];
+        a = part == 0 ? m * inv_sqrt_d : part == 1 ? beta_over_d * qv[gq * D + t] : beta_over_d * (m * m);
       }
+      if (gk < nk) {
+        const double m = km[gk * D + t];
+        bb = part == 0 ? m : part == 1 ? fma(m, m, kv[gk * D + t]) : kv[gk * D + t];
+      }
+      As[buf][lf + e][lr] = a;
+      Bs[buf][lf + e][lr] = bb;
     }
-    __syncthreads();
+  };
+  load(0, 0);
+  __syncthreads();
+  int buf = 0;
+  for (int c0 = 0; c0 < nfeat; c0 += kScK) {
+    if (c0 + kScK < nfeat) load(c0 + kScK, buf ^ 1);  // prefetch the next stage
 #pragma unroll
     for (int k = 0; k < kScK; ++k) {
-      double a[4], bb[4];
+      double a[8], bb[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) { a[i] = As[k][ty * 4 + i]; bb[i] = Bs[k][tx * 4 + i]; }
+      for (int i = 0; i < 4; ++i) {
+        // rows ty*4 .. ty*4+3 and 64 + ty*4 .. : conflict-free 2 x 32-byte reads per operand
+        a[i] = As[buf][k][ty * 4 + i];
+        a[4 + i] = As[buf][k][64 + ty * 4 + i];
+        bb[i] = Bs[buf][k][tx * 4 + i];
+        bb[4 + i] = Bs[buf][k][64 + tx * 4 + i];
+      }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
     }
     __syncthreads();
+    buf ^= 1;
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t gq = gq0 + ty * 4 + i;
+  for (int i = 0; i < 8; ++i) {
+    const int64_t gq = gq0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
     if (gq >= nq) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t gk = gk0 + tx * 4 + j;
+    for (int j = 0; j < 8; ++j) {
+      const int64_t gk = gk0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
       if (gk < nk) logits[(bhq * nq + gq) * nk + gk] = acc[i][j];
     }
   }
@@ -499,6 +548,7 @@ __global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, const doubl
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  unsigned *hist_base = reinterpret_cast<unsigned *>(smem_raw + (size_t)(blockDim.x >> 5) * nk * sizeof(double));
   if (row >= rows) return;
   double *x = reinterpret_cast<double *>(smem_raw) + (int64_t)warp * nk;
   const double *src = logits + row * nk;
@@ -520,29 +570,64 @@ __global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, const doubl
     if (prob)
       for (int64_t j = lane; j < nk; j += 32) prob[row * nk + j] = exp(x[j] - mx) / denom;
   }
-  // kappa-th largest ordered key: greedy MSB-first, keep the largest prefix T
-  // with #(u >= T) >= kappa.
-  uint64_t T = 0;
-  for (int bit = 63; bit >= 0; --bit) {
-    const uint64_t cand = T | (1ull << bit);
-    unsigned cnt = 0;
-    for (int64_t j = lane; j < nk; j += 32) cnt += ordered_bits(x[j]) >= cand;
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if (cnt >= (unsigned)kappa) T = cand;
+  // kappa-th largest ordered key by an 8-pass MSD radix select (8-bit digits):
+  // per pass, histogram the digit of the candidates sharing the current prefix
+  // (per-warp smem histogram), then pick the digit holding the k_rem-th largest.
+  for (int64_t j = lane; j < nk; j += 32)
+    reinterpret_cast<uint64_t *>(x)[j] = ordered_bits(x[j]);  // in place: keys from here on
+  __syncwarp();
+  const uint64_t *u = reinterpret_cast<const uint64_t *>(x);
+  unsigned *hist = hist_base + warp * 256;
+  uint64_t T = 0, pmask = 0;
+  unsigned k_rem = (unsigned)kappa;
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
+    __syncwarp();
+    for (int64_t j = lane; j < nk; j += 32) {
+      const uint64_t v = u[j];
+      if ((v & pmask) == T) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    // lane owns digits [8*lane, 8*lane + 8); suffix sums from the top digit down
+    unsigned c[8], tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { c[i] = hist[lane * 8 + i]; tot += c[i]; }
+    unsigned above = tot;  // inclusive suffix over lanes >= lane
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned o = __shfl_down_sync(0xffffffffu, above, off);
+      if (lane + off < 32) above += o;
+    }
+    above -= tot;  // candidates in digits owned by higher lanes
+    int dsel = -1;
+    unsigned before = 0;
+    unsigned run = above;
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+      if (dsel < 0 && run < k_rem && run + c[i] >= k_rem) { dsel = lane * 8 + i; before = run; }
+      run += c[i];
+    }
+    const unsigned ball = __ballot_sync(0xffffffffu, dsel >= 0);
+    const int owner = __ffs(ball) - 1;
+    dsel = __shfl_sync(0xffffffffu, dsel, owner);
+    before = __shfl_sync(0xffffffffu, before, owner);
+    k_rem -= before;
+    T |= (uint64_t)dsel << shift;
+    pmask |= 0xFFull << shift;
+    __syncwarp();
   }
-  unsigned gt = 0;
-  for (int64_t j = lane; j < nk; j += 32) gt += ordered_bits(x[j]) > T;
-  gt = __reduce_add_sync(0xffffffffu, gt);
-  const unsigned need_eq = (unsigned)kappa - gt;  // >= 1
+  const unsigned need_eq = k_rem;  // equal-to-T entries still needed (>= 1); the rest are > T
   unsigned eq_seen = 0, sel_seen = 0;
   const unsigned lt = lanemask_lt();
   for (int64_t j0 = 0; j0 < nk; j0 += 32) {
     const int64_t j = j0 + lane;
     bool sel = false, eq = false;
     if (j < nk) {
-      const uint64_t u = ordered_bits(x[j]);
-      eq = (u == T);
-      sel = u > T;
+      const uint64_t v = u[j];
+      eq = (v == T);
+      sel = v > T;
     }
     const unsigned eqm = __ballot_sync(0xffffffffu, eq);
     if (eq) sel = (eq_seen + __popc(eqm & lt)) < need_eq;
@@ -555,16 +640,16 @@ __global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, const doubl
   if (lane == 0) kv_count[row] = (int32_t)kappa;
   if (tau && lane == 0) {
     // invert the order-preserving map: T holds the kappa-th largest l' exactly
-    const uint64_t u = (T >> 63) ? (T ^ 0x8000000000000000ull) : ~T;
-    tau[row] = exp(__longlong_as_double((long long)u) - mx) / denom;
+    const uint64_t tb = (T >> 63) ? (T ^ 0x8000000000000000ull) : ~T;
+    tau[row] = exp(__longlong_as_double((long long)tb) - mx) / denom;
   }
 }
 
 cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, const double *logits, int32_t *kv_index,
                         int32_t *kv_count, uint8_t *mask, double *prob, double *tau, cudaStream_t st) {
   int warps = 8;
-  while (warps > 1 && (size_t)warps * nk * sizeof(double) > 160 * 1024) warps >>= 1;
-  const size_t smem = (size_t)warps * nk * sizeof(double);
+  while (warps > 1 && (size_t)warps * (nk * sizeof(double) + 1024) > 160 * 1024) warps >>= 1;
+  const size_t smem = (size_t)warps * (nk * sizeof(double) + 256 * sizeof(unsigned));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
