@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / e2e / cpu legs)")
+    ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
+                    help="batch: weak scaling, rank r runs its own batch element (default); heads: strong "
+                         "scaling, rank r runs a slice of whole GQA groups and O is all-gathered (NCCL)")
     return ap.parse_args()
 
 
@@ -209,7 +212,7 @@ def run_ours(args):
     import torch.distributed as dist
     from synth import CONFIGS, make_qkv
     import paper_2605_19726_b200.baatt as ba
-    from paper_2605_19726_b200.dist import max_over_ranks, sum_over_ranks
+    from paper_2605_19726_b200.dist import gather_heads, head_range, max_over_ranks, sum_over_ranks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -223,9 +226,16 @@ def run_ours(args):
     ba.load()
     w = CONFIGS[args.config]
     density = args.density if args.density is not None else w.density
-    # weak scaling: rank r processes batch element r (its own seeded inputs)
-    wr = w.with_(config_index=w.config_index + 100 * rank)
-    q, k, v = make_qkv(wr, device=dev)
+    heads = args.shard == "heads" and world > 1
+    if heads:
+        # strong scaling: every rank builds the same problem and keeps whole GQA groups
+        q, k, v = make_qkv(w, device=dev)
+        q0, q1, k0, k1 = head_range(w.heads_q, w.heads_kv, world, rank)
+        q, k, v = q[:, q0:q1].contiguous(), k[:, k0:k1].contiguous(), v[:, k0:k1].contiguous()
+    else:
+        # weak scaling: rank r processes batch element r (its own seeded inputs)
+        wr = w.with_(config_index=w.config_index + 100 * rank)
+        q, k, v = make_qkv(wr, device=dev)
     torch.cuda.synchronize()
     ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag")
     out = torch.empty_like(q)
@@ -235,7 +245,10 @@ def run_ours(args):
         ctx.select(q, k, v)
         n_sel = ba.last_launch_count()
         ctx.sparse_attn(out)
-        return n_sel + ba.last_launch_count()
+        n = n_sel + ba.last_launch_count()
+        if heads:
+            gather_heads(out, w.heads_q)  # the path's only collective (NCCL all-gather over NVLink)
+        return n
 
     for _ in range(max(args.warmup, 1)):
         launches = step()
@@ -260,6 +273,8 @@ def run_ours(args):
         ev[i][1].record(stream)
         ctx.sparse_attn(out)
         ev[i][2].record(stream)
+        if heads:
+            gather_heads(out, w.heads_q)
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -358,13 +373,16 @@ def run_ours(args):
             traffic = None
 
     if rank == 0:
-        tokens = q.shape[2] * world
+        tokens = q.shape[2] * (1 if heads else world)
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if heads else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": workload_desc(w, density), "global_batch": world, "seq_len": w.seq_len,
-                       "parallelism": f"batch-parallel x{world} (weak scaling, no data-path collective)",
+            "config": {"workload": workload_desc(w, density), "global_batch": 1 if heads else world,
+                       "seq_len": w.seq_len,
+                       "parallelism": (f"head-parallel x{world} (whole GQA groups per rank, NCCL all-gather of O)"
+                                       if heads else f"batch-parallel x{world} (weak scaling, no data-path collective)"),
                        "l2": "inputs larger than L2 (q+k+v = %.2f GB per step)" %
                              ((q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
             "roofline": {"bound": "tensor", "kernel": "attn_sm100_tcgen05", "achieved": attn_tflops,

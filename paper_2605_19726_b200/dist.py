@@ -41,14 +41,15 @@ def gather_heads(out_local: torch.Tensor, heads_q: int, group=None) -> torch.Ten
     heads (the only collective of the path), else all_gather of padded slices."""
     world = dist.get_world_size(group)
     b, hr, L, d = out_local.shape
-    if hr * world == heads_q:
+    if hr * world == heads_q and dist.get_backend(group) == "nccl":
         # gather along a leading dim, then move heads into place
         flat = out_local.transpose(0, 1).contiguous()  # [hr, b, L, d]
         full = torch.empty((world * hr, b, L, d), dtype=out_local.dtype, device=out_local.device)
         dist.all_gather_into_tensor(full, flat, group=group)
         return full.transpose(0, 1).contiguous()
-    counts = [None] * world
-    dist.all_gather_object(counts, hr, group=group)
+    counts_t = [torch.zeros(1, dtype=torch.int64, device=out_local.device) for _ in range(world)]
+    dist.all_gather(counts_t, torch.tensor([hr], dtype=torch.int64, device=out_local.device), group=group)
+    counts = [int(c.item()) for c in counts_t]
     hmax = max(counts)
     pad = torch.zeros((hmax, b, L, d), dtype=out_local.dtype, device=out_local.device)
     pad[:hr] = out_local.transpose(0, 1)

@@ -1,0 +1,71 @@
+"""Multi-process host logic of the head-parallel split (gloo, world size 2, CPU).
+
+The CUDA kernels cannot run here; these tests cover what the multi-GPU path
+adds on top of them: the head partition (whole GQA groups per rank), the
+output reassembly collective, and the max/sum-over-ranks timing reductions
+bench.py uses.
+"""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2605_19726_b200.dist import gather_heads, head_range, max_over_ranks, sum_over_ranks
+
+
+def test_head_range_partitions():
+    for hq, hkv in ((32, 8), (32, 32), (28, 28), (24, 24), (12, 3)):
+        for world in (1, 2, 3, 4, 8):
+            if world > hkv:
+                continue
+            got_q, got_kv = [], []
+            for r in range(world):
+                q0, q1, k0, k1 = head_range(hq, hkv, world, r)
+                got_q += list(range(q0, q1))
+                got_kv += list(range(k0, k1))
+                # every q-head of the slice reads a kv-head of the slice (whole GQA groups)
+                grp = hq // hkv
+                assert all(k0 <= h // grp < k1 for h in range(q0, q1))
+            assert got_q == list(range(hq)) and got_kv == list(range(hkv))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, hq, hkv, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        b, L, d = 2, 5, 4
+        full = torch.arange(b * hq * L * d, dtype=torch.float32).reshape(b, hq, L, d)
+        q0, q1, _, _ = head_range(hq, hkv, world, rank)
+        got = gather_heads(full[:, q0:q1].contiguous(), hq)
+        ok = torch.equal(got, full)
+        mx = max_over_ranks(float(rank + 1), "cpu")
+        sm = sum_over_ranks(float(rank + 1), "cpu")
+        q.put((rank, ok, mx, sm))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (6, 3)])
+def test_gather_heads_world2(hq, hkv):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, hq, hkv, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _, _ in res), res
+    assert all(mx == 2.0 and sm == 3.0 for _, _, mx, sm in res), res

@@ -1,0 +1,89 @@
+"""Full-size parity at the BASELINE.json configurations, in the launch
+configuration bench.py times (Context.select + Context.sparse_attn on the full
+tensors).
+
+The oracle cannot run every head of a 128K problem in seconds, so:
+  * selection (P1, P4) is checked in full for sampled q-heads (first and last,
+    i.e. different GQA groups), every query block of those heads;
+  * outputs (P5) are checked on sampled query blocks of those heads — block 0,
+    the last (ragged for config V) block, the block with the most
+    near-threshold entries and a seeded random one — computed by the oracle
+    one block at a time with the GPU's permutations and index lists;
+  * properties that hold at any size are checked on the whole output:
+    kv_count == kappa, index rows strictly ascending and in range, finite
+    output, permutations are bijections.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import CONFIGS, make_qkv
+
+from parity import MASK_BAND, TOL, check_selection, oracle_select_all
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def ba():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2605_19726_b200.baatt as ba
+    ba.load()
+    return ba
+
+
+def _blocks_to_check(ref, nq, seed):
+    near = (np.abs(ref.m - ref.tau[:, None]) <= 1e-4).sum(axis=1)
+    rng = np.random.default_rng(seed)
+    return sorted({0, nq - 1, int(near.argmax()), int(rng.integers(nq))})
+
+
+@pytest.mark.parametrize("cfg,density", [("A", 0.5), ("C", 0.5), ("C", 0.25), ("V", 0.5), ("M", 0.5)])
+def test_fullsize(ba, cfg, density):
+    w = CONFIGS[cfg]
+    torch.cuda.empty_cache()
+    q, k, v = make_qkv(w, device="cuda")
+    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag")
+    out = torch.empty_like(q)
+    sel = ctx.select(q, k, v)
+    ctx.sparse_attn(out)
+    torch.cuda.synchronize()
+    kappa, nq, nk = sel.kappa, sel.n_q, sel.n_k
+    # ---- properties over the whole problem
+    assert (sel.kv_count == kappa).all()
+    idx = sel.kv_index.long()
+    assert (idx >= 0).all() and (idx < nk).all()
+    assert (idx[..., 1:] > idx[..., :-1]).all()
+    assert torch.isfinite(out.float()).all()
+    for perm in (sel.perm_q, sel.perm_k):
+        srt = torch.sort(perm.long(), dim=-1).values
+        assert torch.equal(srt, torch.arange(perm.shape[-1], device="cuda").expand_as(srt))
+    # ---- selection of sampled heads vs the oracle (every query block)
+    heads = sorted({0, w.heads_q - 1})
+    ref = oracle_select_all(q, k, w.block_size, density, 1.0, "qk", "diag", heads=heads)
+    rep = check_selection(sel, ref)
+    # ---- sampled output blocks vs the oracle (GPU perm + index lists)
+    grp = w.heads_q // w.heads_kv
+    scale = 1.0 / math.sqrt(w.head_dim)
+    worst = 0.0
+    for h in heads:
+        hk = h // grp
+        pq = sel.perm_q[0, h].cpu().numpy()
+        pk = sel.perm_k[0, hk].cpu().numpy()
+        kvi = sel.kv_index[0, h].cpu().numpy()
+        Qs = O.apply_permutation(q[0, h].cpu(), pq)
+        Ks = O.apply_permutation(k[0, hk].cpu(), pk)
+        Vs = O.apply_permutation(v[0, hk].cpu(), pk)
+        blocks = _blocks_to_check(ref[(0, h)], nq, seed=h)
+        Os, _ = O.block_sparse_attention_head(Qs, Ks, Vs, kvi, w.block_size, scale, blocks)
+        gout = out[0, h].float().cpu().numpy()
+        for g in blocks:
+            s, e = g * w.block_size, min((g + 1) * w.block_size, q.shape[2])
+            rows = pq[s:e]  # original positions of the sorted rows of this block
+            err = np.abs(gout[rows] - Os[s:e]).max()
+            worst = max(worst, float(err))
+    assert worst <= TOL[q.dtype], (worst, rep)
