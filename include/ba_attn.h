@@ -195,9 +195,10 @@ ba_status ba_attention_host(const ba_problem *prob, const ba_params *params,
                             cudaStream_t stream);
 
 /* Name of the attention kernel ba_sparse_attn / ba_attention / ba_dense_attn
- * run for this problem: "attn_sm100_tcgen05" (bf16, d = 128, B = 128: tcgen05
- * tensor cores, TMA, TMEM) or "attn_simt" (fp32 inputs, and bf16 shapes the
- * tensor-core kernel does not cover yet).  "" on an invalid problem. */
+ * run for this problem: "attn_sm100_tcgen05" (bf16, d = 128, B in {64, 128}:
+ * tcgen05 tensor cores, TMA, TMEM; B = 64 pairs two query blocks per 128-row
+ * tile) or "attn_simt" (fp32 inputs, and bf16 d = 64).  "" on an invalid
+ * problem. */
 const char *ba_attention_kernel_name(const ba_problem *prob, const ba_params *params);
 
 /* Number of kernel launches the last successful call on this thread enqueued. */

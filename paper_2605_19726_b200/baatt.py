@@ -18,7 +18,7 @@ from typing import Optional
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbaatt.so")
+LIB_PATH = os.environ.get("BA_LIB_PATH") or os.path.join(HERE, "libbaatt.so")  # override: A/B builds only
 
 BA_DTYPE_BF16, BA_DTYPE_FP32 = 0, 1
 SORT = {"none": 0, "q": 1, "k": 2, "qk": 3}

@@ -1,29 +1,38 @@
 // attn_sm100.cu — K5: block-sparse attention on the 5th-generation tensor
 // cores of sm_100a (tcgen05 + TMEM + TMA).
 //
-// Computes Alg. 1 steps 11-12: for the query block g_q
-// of one (batch, head), O'_{g_q} = softmax(Q'_{g_q} K'_S^T * scale) V'_S over
-// the key blocks S = {g_k : M_{g_q,g_k} = 1} only,
-// renormalised over that support, then rows are written to the original
-// positions pi_q(i).  Non-causal.
+// Computes Alg. 1 steps 11-12: for a query block g_q of
+// one (batch, head), O'_{g_q} = softmax(Q'_{g_q} K'_S^T * scale) V'_S over the
+// key blocks S = {g_k : M_{g_q,g_k} = 1} only, renormalised
+// over that support, then rows are written to the original positions pi_q(i)
+// (P:566).  Non-causal.
 //
-// One CTA per query block (B = 128 rows, d = 128), 11 warps:
-//   warps 0,10 TMA producers: K_j (warp 0) and V_j (warp 10) of the j-th
-//              selected key block (index list kv_index) into independent
-//              4-stage (K) and 2-stage (V) rings (128-byte swizzle).
-//   warp 1     MMA issuer (one thread) and TMEM owner.  S_j = Q K_j^T with Q
-//              held in TMEM (TS form: smem carries only K and V), into a
-//              double-buffered TMEM accumulator, then O += P_j V_j with P_j
-//              read from TMEM — S_{j+1} overlaps the softmax of tile j.
-//   warps 2-9  two softmax warpgroups; warpgroup h owns columns [64h, 64h+64)
-//              of every row (one thread per row and half), so each SMSP runs
-//              two softmax warps.  The halves swap partial row maxima once per
-//              tile through smem + a 64-thread named barrier; online softmax
-//              in the exp2 domain (FFMA2 / FMNMX3 / FADD2, part of the exp2 on
-//              the FMA pipe), lazy O rescaling (only when the running max grows
-//              by > 2^8), P_j (bf16) written back over S_j in TMEM; epilogue
-//              O / l -> bf16 rows at pi_q(i), plus optional LSE.
-// TMEM columns: S0 [0,128), S1 [128,256), O [256,384), Q [384,448).
+// One CTA per 128-row query tile, templated on the key-block size kBN = B:
+//   B = 128: the tile is one query block; it walks that block's index list.
+//   B = 64:  the tile is a PAIR of adjacent query blocks (2p, 2p+1); it walks
+//            the union of their two lists and every key tile is loaded once
+//            for both; rows of a block that did not select the current key
+//            block get P = 0.  (tcgen05 M = 128 at half the rows would waste
+//            half the tensor pipe; the pair recovers it where lists overlap.)
+// 11 warps:
+//   warps 0,10 TMA producers: K_u (warp 0) and V_u (warp 10) of the u-th key
+//              block of the (union) list into independent rings (128-byte
+//              swizzle, two 64-column boxes per tile).
+//   warp 1     MMA issuer (one elected thread) and TMEM owner.  S_u = Q K_u^T
+//              with Q held in TMEM (TS form: smem carries only K and V), into
+//              a double-buffered TMEM accumulator, then O += P_u V_u with P_u
+//              read from TMEM — S_{u+1} overlaps the softmax of tile u.
+//   warps 2-9  two softmax warpgroups; warpgroup h owns columns
+//              [h*B/2, (h+1)*B/2) of every row (one thread per row and half),
+//              two softmax warps per SMSP.  The halves swap partial row maxima
+//              once per tile through smem + a 64-thread named barrier; online
+//              softmax in the exp2 domain (FFMA2 / FMNMX3 / FADD2), lazy O
+//              rescaling (only when the running max grows by > 2^8), P_u (bf16)
+//              written back over S_u in TMEM; epilogue O / l -> bf16 rows at
+//              pi_q(i), plus optional LSE.
+// The key-block list is turned into an smem bitmask once per CTA (union of
+// the pair's lists for B = 64); every role enumerates its set bits in order.
+// TMEM columns: S0 [0,B), S1 [B,2B), O [256,384), Q [384,448).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <math.h>
@@ -36,37 +45,51 @@
 namespace baatt {
 namespace sm100 {
 
-constexpr int BM = 128;          // query rows per tile (= block size B)
-constexpr int BN = 128;          // key rows per tile
+constexpr int BM = 128;          // query rows per tile
 constexpr int HD = 128;          // head dim
-constexpr int NKS = 4;           // K stages
-constexpr int NVS = 2;           // V stages (V is consumed a tile after K)
-constexpr uint32_t BOX_BYTES = 128 * 64 * 2;     // one 128-row x 64-col bf16 box (16 KB)
-constexpr uint32_t TILE_BYTES = 2 * BOX_BYTES;   // 128 x 128 bf16 (32 KB)
-BA_DEVICE constexpr uint32_t s_col(int buf) { return buf ? 128u : 0u; }
 constexpr uint32_t O_COL = 256;
 constexpr uint32_t Q_COL = 384;
 constexpr int kSoftmaxWarp0 = 2;
 constexpr int kVProducerWarp = 10;
 constexpr int kThreads = 352;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-constexpr int kDefaultEmu = 0;             // pairs per 8 on the polynomial exp2
+constexpr int kDefaultEmu = 0;             // pairs per 8 on the polynomial exp2 (off: MUFU + power cap wins)
+constexpr int kMaskWords = 1024;           // bitmask capacity: N_k <= 32768 key blocks
 
-struct __align__(8) Bars {
+template <int kBN>
+struct Cfg {
+  static constexpr uint32_t BOX_BYTES = kBN * 64 * 2;      // kBN rows x 64 bf16 columns
+  static constexpr uint32_t TILE_BYTES = 2 * BOX_BYTES;    // kBN x 128
+  static constexpr int NKS = 4 * (128 / kBN);              // K stages (same bytes for both B)
+  static constexpr int NVS = 2 * (128 / kBN);              // V stages (V is consumed a tile after K)
+  static constexpr int HC = kBN / 2;                       // S columns per softmax half
+  static constexpr bool kPair = kBN == 64;
+  // instruction descriptors, kind::f16: D fp32, A/B bf16, dense, M = 128
+  static constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                                      ((uint32_t)(BM >> 4) << 24);                    // A K-major (Q), B K-major (K)
+  static constexpr uint32_t IDESC_O = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(HD >> 3) << 17) |
+                                      ((uint32_t)(BM >> 4) << 24) | (1u << 16);       // B MN-major (V: d contiguous)
+  static constexpr uint32_t SMEM_K = 0;
+  static constexpr uint32_t SMEM_V = SMEM_K + NKS * TILE_BYTES;
+  static constexpr uint32_t SMEM_RED = SMEM_V + NVS * TILE_BYTES;     // float [2][2][128] row-max exchange
+  static constexpr uint32_t SMEM_RED2 = SMEM_RED + 2 * 2 * 128 * 4;   // float [2][128] final l exchange
+  static constexpr uint32_t SMEM_MASK = SMEM_RED2 + 2 * 128 * 4;      // uint32 [2][kMaskWords]
+  static constexpr uint32_t SMEM_BARS = SMEM_MASK + 2 * kMaskWords * 4;
+  static constexpr uint32_t SMEM_BYTES = SMEM_BARS + 512 + 1024;     // + alignment slack
+  static __device__ constexpr uint32_t s_col(int buf) { return buf ? (uint32_t)kBN : 0u; }
+};
+
+template <int NKS, int NVS>
+struct __align__(8) BarsT {
   uint64_t q_full;
   uint64_t k_full[NKS], k_empty[NKS];
   uint64_t v_full[NVS], v_empty[NVS];
   uint64_t s_full[2], p_full[2];
   uint64_t o_done;
   uint32_t tmem_base;
+  uint32_t n_union;
+  uint32_t last_ragged;
 };
-
-constexpr uint32_t SMEM_K = 0;
-constexpr uint32_t SMEM_V = SMEM_K + NKS * TILE_BYTES;
-constexpr uint32_t SMEM_RED = SMEM_V + NVS * TILE_BYTES;       // float [2][2][128] row-max exchange
-constexpr uint32_t SMEM_RED2 = SMEM_RED + 2 * 2 * 128 * 4;     // float [2][128] final l exchange
-constexpr uint32_t SMEM_BARS = SMEM_RED2 + 2 * 128 * 4;
-constexpr uint32_t SMEM_BYTES = SMEM_BARS + 256 + 1024;       // + alignment slack
 
 // ------------------------------------------------------------------ PTX wrappers
 BA_DEVICE uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -97,6 +120,7 @@ BA_DEVICE void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync
 BA_DEVICE void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 BA_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 BA_DEVICE void named_bar_sync(int id, int count) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory"); }
+
 
 BA_DEVICE void tma_prefetch(const CUtensorMap *m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
@@ -202,33 +226,45 @@ BA_DEVICE uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return d;
 }
 
-// Instruction descriptor, kind::f16: D fp32, A/B bf16, dense, M = 128, N = 128.
-constexpr uint32_t IDESC_BASE = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-constexpr uint32_t IDESC_S = IDESC_BASE;              // A K-major (Q), B K-major (K)
-constexpr uint32_t IDESC_O = IDESC_BASE | (1u << 16); // B MN-major (V: d contiguous)
 
-// kEmu: of every 8 element pairs of a row tile, how many take the polynomial
-// exp2 (FMA pipe) instead of MUFU.EX2.
+// Ordered walk over the set bits of (A | B).
+struct UnionWalk {
+  const uint32_t *ma, *mb;
+  int w;
+  uint32_t rem;
+  BA_DEVICE void init(const uint32_t *a_, const uint32_t *b_) { ma = a_; mb = b_; w = 0; rem = a_[0] | b_[0]; }
+  BA_DEVICE int next() {
+    while (rem == 0) { ++w; rem = ma[w] | mb[w]; }
+    const int bit = __ffs(rem) - 1;
+    rem &= rem - 1;
+    return w * 32 + bit;
+  }
+};
+
 // kNoSoftmax: profiling-only variant (BA_ATTN_DEBUG=1) in which the softmax
 // warps hand S straight back without touching it — it measures the MMA + TMA
 // pipeline ceiling; its output is meaningless.
-// kTrace: profiling-only variant (BA_ATTN_TRACE=1): CTA (0,0) records clock64
-// timestamps of the first kTraceTiles tiles for the producer, MMA and one
-// softmax warp of each half, and prints them.
+// kTrace: profiling-only variant (BA_ATTN_DEBUG=2): CTA (0,0) records clock64
+// timestamps of the first kTraceTiles tiles for the producers, the MMA issuer
+// and one softmax warp of each half, and prints them.
 constexpr int kTraceTiles = 12;
-template <int kEmu, bool kNoSoftmax = false, bool kTrace = false>
+template <int kBN, int kEmu, bool kNoSoftmax = false, bool kTrace = false>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
+  using C = Cfg<kBN>;
+  using Bars = BarsT<C::NKS, C::NVS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t *smem = smem_raw + (base - raw);
-  Bars &bars = *reinterpret_cast<Bars *>(smem + SMEM_BARS);
-  float *red = reinterpret_cast<float *>(smem + SMEM_RED);    // [2][2][128]
-  float *red2 = reinterpret_cast<float *>(smem + SMEM_RED2);  // [2][128]
+  Bars &bars = *reinterpret_cast<Bars *>(smem + C::SMEM_BARS);
+  float *red = reinterpret_cast<float *>(smem + C::SMEM_RED);    // [2][2][128]
+  float *red2 = reinterpret_cast<float *>(smem + C::SMEM_RED2);  // [2][128]
+  uint32_t *mask_a = reinterpret_cast<uint32_t *>(smem + C::SMEM_MASK);
+  uint32_t *mask_b = mask_a + kMaskWords;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gq = blockIdx.x;
+  const int tile = blockIdx.x;  // 128-row query tile (one block for B = 128, a pair for B = 64)
   const int64_t bh = blockIdx.y;
   __shared__ long long trace[16][kTraceTiles];
   const bool tr = kTrace && blockIdx.x == 0 && blockIdx.y == 0;
@@ -236,19 +272,53 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
 #define TR(slot, j) do { if (tr && (j) < kTraceTiles) trace[slot][j] = clock64() - t_origin; } while (0)
   const int64_t b = bh / a.hq, h = bh - b * a.hq;
   const int64_t hk = h / (a.hq / a.hkv);
-  const int64_t row = bh * a.nq + gq;
-  const int cnt = a.kv_index ? (a.kv_count ? a.kv_count[row] : (int)a.kv_stride) : (int)a.nk;
-  const int32_t *idx = a.kv_index ? a.kv_index + row * a.kv_stride : nullptr;
+  const int nw = (int)((a.nk + 31) >> 5);
+
+  // ---- key-block set of this tile as bitmasks (block A = first query block, B = second for pairs)
+  const int64_t ga = C::kPair ? 2 * (int64_t)tile : tile;
+  const bool has_b = C::kPair && ga + 1 < a.nq;
+  for (int w = threadIdx.x; w < 2 * kMaskWords; w += kThreads) mask_a[w] = 0u;
+  __syncthreads();
+  for (int q2 = 0; q2 < (has_b ? 2 : 1); ++q2) {
+    const int64_t row = bh * a.nq + ga + q2;
+    uint32_t *m = q2 ? mask_b : mask_a;
+    if (a.kv_index) {
+      const int cnt = a.kv_count ? a.kv_count[row] : (int)a.kv_stride;
+      const int32_t *idx = a.kv_index + row * a.kv_stride;
+      for (int e = threadIdx.x; e < cnt; e += kThreads) {
+        const int g = idx[e];
+        atomicOr(&m[g >> 5], 1u << (g & 31));
+      }
+    } else {  // dense: every key block
+      for (int w = threadIdx.x; w < nw; w += kThreads)
+        m[w] = (w + 1) * 32 <= a.nk ? 0xffffffffu : ((1u << (a.nk & 31)) - 1u);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {  // |A u B| = number of key tiles this CTA streams
+    unsigned c = 0;
+    for (int w = lane; w < nw; w += 32) c += __popc(mask_a[w] | mask_b[w]);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) {
+      bars.n_union = c;
+      // a ragged last key block, when selected, is always the last tile of the ascending walk
+      const int64_t gl = a.nk - 1;
+      const bool sel_last = ((mask_a[gl >> 5] | mask_b[gl >> 5]) >> (gl & 31)) & 1u;
+      bars.last_ragged = sel_last && (a.lk - gl * (int64_t)kBN) < kBN;
+    }
+  }
+  __syncthreads();
+  const int cnt = (int)bars.n_union;
 
   if (warp == 0 && lane == 0) {
     mbar_init(&bars.q_full, 8);   // one elected arrive per softmax warp
-    for (int s = 0; s < NKS; ++s) { mbar_init(&bars.k_full[s], 1); mbar_init(&bars.k_empty[s], 1); }
-    for (int s = 0; s < NVS; ++s) { mbar_init(&bars.v_full[s], 1); mbar_init(&bars.v_empty[s], 1); }
+    for (int s = 0; s < C::NKS; ++s) { mbar_init(&bars.k_full[s], 1); mbar_init(&bars.k_empty[s], 1); }
+    for (int s = 0; s < C::NVS; ++s) { mbar_init(&bars.v_full[s], 1); mbar_init(&bars.v_empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&bars.s_full[s], 1); mbar_init(&bars.p_full[s], 8); }
     mbar_init(&bars.o_done, 1);
     fence_barrier_init();
     tma_prefetch(&tm_k);
-    tma_prefetch(&tm_v);  // (both producers read their own map)
+    tma_prefetch(&tm_v);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&bars.tmem_base)), "r"(512));
@@ -261,25 +331,27 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
 
   if (warp == 0 || warp == kVProducerWarp) {
     // ================================================================ TMA producers
-    // warp 0 streams K_j, the last warp streams V_j: independent rings, so a
+    // warp 0 streams K_u, the last warp streams V_u: independent rings, so a
     // wait for a free V slot never delays the next K load (and vice versa).
     const bool is_k = warp == 0;
-    const int nst = is_k ? NKS : NVS;
+    const int nst = is_k ? C::NKS : C::NVS;
     const CUtensorMap *map = is_k ? &tm_k : &tm_v;
     uint64_t *full = is_k ? bars.k_full : bars.v_full;
     uint64_t *empty = is_k ? bars.k_empty : bars.v_empty;
-    const uint32_t ring = base + (is_k ? SMEM_K : SMEM_V);
+    const uint32_t ring = base + (is_k ? C::SMEM_K : C::SMEM_V);
     if (lane == 0 && cnt > 0) {
+      UnionWalk walk;
+      walk.init(mask_a, mask_b);
       for (int j = 0; j < cnt; ++j) {
+        const int gk = walk.next();
         const int s = j % nst;
         const uint32_t ph = (uint32_t)(j / nst) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
         TR(is_k ? 0 : 1, j);
-        const int gk = idx ? idx[j] : j;
-        const uint32_t dst = ring + s * TILE_BYTES;
-        mbar_expect_tx(&full[s], TILE_BYTES);
-        tma_load_4d(dst, map, &full[s], 0, gk * BN, (int)hk, (int)b);
-        tma_load_4d(dst + BOX_BYTES, map, &full[s], 64, gk * BN, (int)hk, (int)b);
+        const uint32_t dst = ring + s * C::TILE_BYTES;
+        mbar_expect_tx(&full[s], C::TILE_BYTES);
+        tma_load_4d(dst, map, &full[s], 0, gk * kBN, (int)hk, (int)b);
+        tma_load_4d(dst + C::BOX_BYTES, map, &full[s], 64, gk * kBN, (int)hk, (int)b);
       }
     }
     __syncwarp();
@@ -289,15 +361,16 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       mbar_wait(&bars.q_full, 0);
       tc_fence_after();
       auto issue_s = [&](int j) {
-        const int s = j % NKS;
-        mbar_wait(&bars.k_full[s], (uint32_t)(j / NKS) & 1u);
+        const int s = j % C::NKS;
+        mbar_wait(&bars.k_full[s], (uint32_t)(j / C::NKS) & 1u);
         TR(2, j);
         tc_fence_after();
-        const uint32_t sk = base + SMEM_K + s * TILE_BYTES;
+        const uint32_t sk = base + C::SMEM_K + s * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * BOX_BYTES + (kk & 3) * 32;
-          mma_ts(tmem + s_col(j & 1), tmem + Q_COL + kk * 8, make_desc(sk + off, 16, 1024), IDESC_S, kk > 0 ? 1u : 0u);
+          const uint32_t off = (kk >> 2) * C::BOX_BYTES + (kk & 3) * 32;
+          mma_ts(tmem + C::s_col(j & 1), tmem + Q_COL + kk * 8, make_desc(sk + off, 16, 1024), C::IDESC_S,
+                 kk > 0 ? 1u : 0u);
         }
         mma_commit(&bars.k_empty[s]);
         mma_commit(&bars.s_full[j & 1]);
@@ -307,15 +380,15 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
         if (j + 1 < cnt) issue_s(j + 1);
         mbar_wait(&bars.p_full[j & 1], (uint32_t)(j >> 1) & 1u);
         TR(3, j);
-        const int s = j % NVS;
-        mbar_wait(&bars.v_full[s], (uint32_t)(j / NVS) & 1u);
+        const int s = j % C::NVS;
+        mbar_wait(&bars.v_full[s], (uint32_t)(j / C::NVS) & 1u);
         TR(4, j);
         tc_fence_after();
-        const uint32_t sv = base + SMEM_V + s * TILE_BYTES;
+        const uint32_t sv = base + C::SMEM_V + s * C::TILE_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          mma_ts(tmem + O_COL, tmem + s_col(j & 1) + kk * 8, make_desc(sv + kk * 2048, BOX_BYTES, 1024), IDESC_O,
-                 (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          mma_ts(tmem + O_COL, tmem + C::s_col(j & 1) + kk * 8, make_desc(sv + kk * 2048, C::BOX_BYTES, 1024),
+                 C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(&bars.v_empty[s]);
         mma_commit(&bars.o_done);
@@ -324,13 +397,16 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
     __syncwarp();
   } else if (warp >= kSoftmaxWarp0 && warp < kSoftmaxWarp0 + 8) {
     // ================================================================ softmax + epilogue
+    constexpr int HC = C::HC;
     const int sw = warp - kSoftmaxWarp0;  // 0..7
     const int hf = sw >> 2;               // column half owned by this warpgroup
     const int qd = warp & 3;              // TMEM lane quadrant of this warp
     const int r = qd * 32 + lane;         // query row within the tile
     const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
-    const int64_t row0 = (int64_t)gq * BM;
+    const int64_t row0 = (int64_t)tile * BM;
     const int nrows = (int)imin64(BM, a.lq - row0);
+    // which query block of the tile this warp's rows belong to (pairs: rows 0-63 -> A, 64-127 -> B)
+    const uint32_t *my_mask = (C::kPair && qd >= 2) ? mask_b : mask_a;
     // Q row half -> TMEM (A operand of S = Q K^T): element pairs packed per column
     {
       uint32_t qv[32];
@@ -348,11 +424,18 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       if (lane == 0) mbar_arrive(&bars.q_full);
     }
     const float c = a.scale * 1.4426950408889634f;  // scale * log2(e)
-    const int64_t ragged_valid = a.lk - (a.nk - 1) * (int64_t)BN;  // rows in the last key block
-    const bool ragged = ragged_valid < BN;
+    const int64_t ragged_valid = a.lk - (a.nk - 1) * (int64_t)kBN;  // rows in the last key block
     float m = -INFINITY, l = 0.f;
-    uint32_t sr[64];
+    uint32_t sr[HC];
+    const bool last_ragged = bars.last_ragged != 0u;
+    UnionWalk walk;  // only pairs need the per-tile block (row-half membership)
+    if constexpr (C::kPair) walk.init(mask_a, mask_b);
     for (int j = 0; j < cnt; ++j) {
+      bool mine = true;
+      if constexpr (C::kPair) {
+        const int gk = walk.next();
+        mine = (my_mask[gk >> 5] >> (gk & 31)) & 1u;  // warp-uniform
+      }
       mbar_wait(&bars.s_full[j & 1], (uint32_t)(j >> 1) & 1u);
       if (lane == 0 && qd == 0) TR(5 + 5 * hf, j);
       tc_fence_after();
@@ -362,81 +445,88 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
         if (lane == 0) mbar_arrive(&bars.p_full[j & 1]);
         continue;
       }
-      tmem_ld_x32(trow + s_col(j & 1) + hf * 64, sr);
-      tmem_ld_x32(trow + s_col(j & 1) + hf * 64 + 32, sr + 32);
-      tmem_wait_ld();
-      if (lane == 0 && qd == 0) TR(6 + 5 * hf, j);
-      if (ragged) {
-        const int gk = idx ? idx[j] : j;
-        if (gk == a.nk - 1) {
+      if (mine) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (hf * 64 + i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
+        for (int q2 = 0; q2 < HC / 32; ++q2) tmem_ld_x32(trow + C::s_col(j & 1) + hf * HC + q2 * 32, sr + q2 * 32);
+        tmem_wait_ld();
+        if (last_ragged && j == cnt - 1) {
+#pragma unroll
+          for (int i = 0; i < HC; ++i)
+            if (hf * HC + i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
         }
       }
-      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      if (lane == 0 && qd == 0) TR(6 + 5 * hf, j);
+      float pmax = -INFINITY;
+      if (mine) {
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int i = 0; i < 64; i += 8) {
+        for (int i = 0; i < HC; i += 8) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          m4[u] = fmax3(m4[u], __uint_as_float(sr[i + 2 * u]), __uint_as_float(sr[i + 2 * u + 1]));
+          for (int u = 0; u < 4; ++u)
+            m4[u] = fmax3(m4[u], __uint_as_float(sr[i + 2 * u]), __uint_as_float(sr[i + 2 * u + 1]));
+        }
+        pmax = fmaxf(fmax3(m4[0], m4[1], m4[2]), m4[3]);
       }
-      const float pmax = fmaxf(fmax3(m4[0], m4[1], m4[2]), m4[3]);
-      // swap partial maxima with the other half of the row (red is double-buffered by j)
+      // swap partial maxima with the other half of the row (red is double-buffered by j;
+      // every tile passes the barrier, selected or not, so the buffer reuse stays safe)
       red[((j & 1) * 2 + hf) * 128 + r] = pmax;
       tc_fence_before();
       named_bar_sync(1 + qd, 64);
       tc_fence_after();
       if (lane == 0 && qd == 0) TR(7 + 5 * hf, j);
-      const float mt = fmaxf(pmax, red[((j & 1) * 2 + (hf ^ 1)) * 128 + r]) * c;
-      if (j == 0) {
-        m = mt;
-      } else {
-        const bool need = mt > m + kRescaleThreshold;
-        if (__any_sync(0xffffffffu, need)) {  // same rows -> same decision in both halves
-          float corr = 1.f;
-          if (need) { corr = ex2(m - mt); m = mt; }
-          mbar_wait(&bars.o_done, (uint32_t)(j - 1) & 1u);
-          tc_fence_after();
-          uint32_t ov[32];
-#pragma unroll
-          for (int q2 = 0; q2 < 2; ++q2) {
-            tmem_ld_x32(trow + O_COL + hf * 64 + q2 * 32, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
-            tmem_st_x32(trow + O_COL + hf * 64 + q2 * 32, ov);
-          }
-          l *= corr;
-        }
-      }
-      // p = 2^(s*c - m): FFMA2 for the argument, MUFU or polynomial exp2, FADD2 row sums
-      const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
-      uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
-        uint64_t p2;
-        if ((i & 7) < kEmu) {
-          p2 = exp2_poly2(x2);
+      if (mine) {
+        const float mt = fmaxf(pmax, red[((j & 1) * 2 + (hf ^ 1)) * 128 + r]) * c;
+        if (m == -INFINITY) {
+          m = mt;  // first tile of these rows: O rows are still zero (earlier P rows were 0)
         } else {
-          float x0, x1;
-          unf2(x2, x0, x1);
-          p2 = f2(ex2(x0), ex2(x1));
+          const bool need = mt > m + kRescaleThreshold;
+          if (__any_sync(0xffffffffu, need)) {  // same rows -> same decision in both halves
+            float corr = 1.f;
+            if (need) { corr = ex2(m - mt); m = mt; }
+            mbar_wait(&bars.o_done, (uint32_t)(j - 1) & 1u);
+            tc_fence_after();
+            uint32_t ov[16];
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+              tmem_ld_x16(trow + O_COL + hf * 64 + q2 * 16, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
+              tmem_st_x16(trow + O_COL + hf * 64 + q2 * 16, ov);
+            }
+            l *= corr;
+          }
         }
-        acc2[i & 3] = fadd2(acc2[i & 3], p2);
-        float p0, p1;
-        unf2(p2, p0, p1);
-        sr[i] = pack_bf16(p0, p1);
-      }
-      {
+        // p = 2^(s*c - m): FFMA2 for the argument, MUFU or polynomial exp2, FADD2 row sums
+        const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int i = 0; i < HC / 2; ++i) {
+          const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
+          uint64_t p2;
+          if ((i & 7) < kEmu) {
+            p2 = exp2_poly2(x2);
+          } else {
+            float x0, x1;
+            unf2(x2, x0, x1);
+            p2 = f2(ex2(x0), ex2(x1));
+          }
+          acc2[i & 3] = fadd2(acc2[i & 3], p2);
+          float p0, p1;
+          unf2(p2, p0, p1);
+          sr[i] = pack_bf16(p0, p1);
+        }
         const uint64_t t2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
         float a0, a1;
         unf2(t2, a0, a1);
         l += a0 + a1;
+      } else {
+#pragma unroll
+        for (int i = 0; i < HC / 2; ++i) sr[i] = 0u;  // block not selected by these rows: P = 0
       }
       if (lane == 0 && qd == 0) TR(8 + 5 * hf, j);
-      tmem_st_x32(trow + s_col(j & 1) + hf * 32, sr);
+      if constexpr (HC / 2 == 32) tmem_st_x32(trow + C::s_col(j & 1) + hf * (HC / 2), sr);
+      else tmem_st_x16(trow + C::s_col(j & 1) + hf * (HC / 2), sr);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();  // all 32 lanes' P stores are complete before the warp's single arrive
@@ -451,7 +541,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       mbar_wait(&bars.o_done, (uint32_t)(cnt - 1) & 1u);
       tc_fence_after();
     }
-    const float inv = cnt > 0 ? 1.f / lt : 0.f;
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
     int64_t orow = row0 + r;
     if (r < nrows && a.perm_q) orow = a.perm_q[bh * a.lq + row0 + r];
     __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(a.out) + b * a.os[0] + h * a.os[1] + orow * a.os[2] + hf * 64;
@@ -470,7 +560,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
         for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
       }
     }
-    if (a.lse && hf == 0 && r < nrows) a.lse[bh * a.lq + orow] = cnt > 0 ? (m + log2f(lt)) * 0.69314718055994531f : -INFINITY;
+    if (a.lse && hf == 0 && r < nrows) a.lse[bh * a.lq + orow] = lt > 0.f ? (m + log2f(lt)) * 0.69314718055994531f : -INFINITY;
   }
   tc_fence_before();
   __syncthreads();
@@ -503,8 +593,9 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 4-D map over a [b, H, L, d] bf16 tensor with element strides (s0, s1, s2), box 64 x 128.
-bool make_map(CUtensorMap *m, const void *ptr, int64_t b, int64_t H, int64_t L, int64_t d, const int64_t *s) {
+// 4-D map over a [b, H, L, d] bf16 tensor with element strides (s0, s1, s2), box 64 x rows.
+bool make_map(CUtensorMap *m, const void *ptr, int64_t b, int64_t H, int64_t L, int64_t d, const int64_t *s,
+              int rows) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)L, (cuuint64_t)H, (cuuint64_t)b};
@@ -512,7 +603,7 @@ bool make_map(CUtensorMap *m, const void *ptr, int64_t b, int64_t H, int64_t L, 
   // a zero / tiny stride on a singleton dim is legal for us but not for TMA: make it dense
   if (H == 1) strides[1] = strides[0] * (cuuint64_t)L;
   if (b == 1) strides[2] = strides[1] * (cuuint64_t)H;
-  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)rows, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -520,64 +611,53 @@ bool make_map(CUtensorMap *m, const void *ptr, int64_t b, int64_t H, int64_t L, 
   return r == CUDA_SUCCESS;
 }
 
+template <int kBN, int kEmu, bool kNoSoftmax, bool kTrace>
+cudaError_t launch_variant(const AttnArgs &a, const CUtensorMap &mk, const CUtensorMap &mv, cudaStream_t st) {
+  using C = Cfg<kBN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel<kBN, kEmu, kNoSoftmax, kTrace>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t tiles = C::kPair ? (a.nq + 1) / 2 : a.nq;
+  dim3 grid((unsigned)tiles, (unsigned)(a.batch * a.hq));
+  attn_sm100_kernel<kBN, kEmu, kNoSoftmax, kTrace><<<grid, kThreads, C::SMEM_BYTES, st>>>(a, mk, mv);
+  return cudaGetLastError();
+}
+
 }  // namespace sm100
 
-bool attn_sm100_supported(const AttnArgs &a) { return a.dtype == 0 && a.d == 128 && a.B == 128; }
+bool attn_sm100_supported(const AttnArgs &a) {
+  return a.dtype == 0 && a.d == 128 && (a.B == 128 || a.B == 64) && a.nk <= 32 * sm100::kMaskWords;
+}
 
 cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
   using namespace sm100;
   CUtensorMap mk, mv;
   if (!get_encode()) return cudaErrorNotSupported;  // no TMA encoder: fail loudly, never fall back
-  if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) || !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs))
+  if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, a.B) ||
+      !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, a.B))
     return cudaErrorInvalidValue;
-  // exp2 offload fraction: compile-time variants, BA_EXP_EMU=0..4 selects one (tuning knob)
-  static int emu = -1;
+  // exp2 offload fraction: compile-time variants, BA_EXP_EMU=0..2 selects one (tuning knob);
+  // BA_ATTN_DEBUG=1 / 2 select the no-softmax / trace profiling variants (B = 128)
+  static int emu = -1, dbg = -1;
   if (emu < 0) {
     const char *env = getenv("BA_EXP_EMU");
     emu = env ? atoi(env) : kDefaultEmu;
-    if (emu < 0 || emu > 4) emu = kDefaultEmu;
+    if (emu < 0 || emu > 2) emu = kDefaultEmu;
+    const char *d = getenv("BA_ATTN_DEBUG");
+    dbg = d ? atoi(d) : 0;
   }
-  dim3 grid((unsigned)a.nq, (unsigned)(a.batch * a.hq));
-#define BA_LAUNCH(E)                                                                                          \
-  do {                                                                                                        \
-    static bool attr = false;                                                                                 \
-    if (!attr) {                                                                                              \
-      cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           (int)SMEM_BYTES);                                                  \
-      if (e != cudaSuccess) return e;                                                                         \
-      attr = true;                                                                                            \
-    }                                                                                                         \
-    attn_sm100_kernel<E><<<grid, kThreads, SMEM_BYTES, st>>>(a, mk, mv);                                  \
-  } while (0)
-  static int dbg = -1;
-  if (dbg < 0) {
-    const char *env = getenv("BA_ATTN_DEBUG");
-    dbg = env ? atoi(env) : 0;
-  }
-  if (dbg == 2) {
-    cudaFuncSetAttribute(attn_sm100_kernel<kDefaultEmu, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    attn_sm100_kernel<kDefaultEmu, false, true><<<grid, kThreads, SMEM_BYTES, st>>>(a, mk, mv);
-    return cudaGetLastError();
-  }
-  if (dbg == 3) {
-    cudaFuncSetAttribute(attn_sm100_kernel<0, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    attn_sm100_kernel<0, true, true><<<grid, kThreads, SMEM_BYTES, st>>>(a, mk, mv);
-    return cudaGetLastError();
-  }
-  if (dbg == 1) {
-    cudaFuncSetAttribute(attn_sm100_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    attn_sm100_kernel<0, true><<<grid, kThreads, SMEM_BYTES, st>>>(a, mk, mv);
-    return cudaGetLastError();
-  }
+  if (a.B == 64) return launch_variant<64, 0, false, false>(a, mk, mv, st);
+  if (dbg == 1) return launch_variant<128, 0, true, false>(a, mk, mv, st);
+  if (dbg == 2) return launch_variant<128, 0, false, true>(a, mk, mv, st);
   switch (emu) {
-    case 0: BA_LAUNCH(0); break;
-    case 1: BA_LAUNCH(1); break;
-    case 2: BA_LAUNCH(2); break;
-    case 4: BA_LAUNCH(4); break;
-    default: BA_LAUNCH(3); break;
+    case 1: return launch_variant<128, 1, false, false>(a, mk, mv, st);
+    case 2: return launch_variant<128, 2, false, false>(a, mk, mv, st);
+    default: return launch_variant<128, 0, false, false>(a, mk, mv, st);
   }
-#undef BA_LAUNCH
-  return cudaGetLastError();
 }
 
 }  // namespace baatt
