@@ -4,7 +4,10 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <algorithm>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/ba_attn.h"
 #include "kernels.h"
@@ -389,11 +392,69 @@ ba_status ba_dense_attn(const ba_problem *prob, const ba_params *params, const v
   return run_attn(a, stream);
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------- host-buffer path
+// ba_attention_host pipelines the transfers against the compute per chunk of
+// KV heads (whole GQA groups, ~8 chunks): H2D of chunk c+1 on one copy stream
+// and D2H of chunk c-1 on another overlap the selection + attention of chunk c
+// on the caller's stream.  The copy streams are created once per device and
+// cached (the library's only mutable state besides kernel attributes).
+namespace {
+
+struct HostPlan {
+  int64_t kv_per_chunk, chunks_per_batch;
+  ba_problem chunk_prob;
+  size_t q_bytes, kv_bytes, ws_chunk;
+};
+
+HostPlan plan_host(const Dims &D, const ba_problem *prob, const ba_params *pa) {
+  HostPlan h{};
+  h.kv_per_chunk = (D.hkv + 7) / 8;
+  h.chunks_per_batch = (D.hkv + h.kv_per_chunk - 1) / h.kv_per_chunk;
+  ba_problem p = *prob;
+  p.batch = 1;
+  p.heads_kv = (int32_t)h.kv_per_chunk;
+  p.heads_q = (int32_t)(h.kv_per_chunk * (D.hq / D.hkv));
+  // strides of the full contiguous staging tensors (a chunk is a contiguous head range)
+  p.q_stride[2] = D.d; p.q_stride[1] = D.lq * D.d; p.q_stride[0] = D.hq * D.lq * D.d;
+  p.k_stride[2] = D.d; p.k_stride[1] = D.lk * D.d; p.k_stride[0] = D.hkv * D.lk * D.d;
+  for (int i = 0; i < 3; ++i) { p.v_stride[i] = p.k_stride[i]; p.o_stride[i] = p.q_stride[i]; }
+  h.chunk_prob = p;
+  h.q_bytes = D.esz * D.b * D.hq * D.lq * D.d;
+  h.kv_bytes = D.esz * D.b * D.hkv * D.lk * D.d;
+  h.ws_chunk = ba_attention_workspace_size(&h.chunk_prob, pa);
+  return h;
+}
+
+std::mutex g_stream_mu;
+cudaStream_t g_copy_streams[64][2];
+
+cudaError_t copy_streams(cudaStream_t *h2d, cudaStream_t *d2h) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lock(g_stream_mu);
+  for (int i = 0; i < 2; ++i)
+    if (!g_copy_streams[dev][i]) {
+      e = cudaStreamCreateWithFlags(&g_copy_streams[dev][i], cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+    }
+  *h2d = g_copy_streams[dev][0];
+  *d2h = g_copy_streams[dev][1];
+  return cudaSuccess;
+}
+
+}  // namespace
+
+extern "C" {
+
 size_t ba_attention_host_workspace_size(const ba_problem *prob, const ba_params *params) {
   Dims D;
   if (check_problem(prob, params, &D) != BA_OK) return 0;
-  const size_t q = align_up(D.esz * D.b * D.hq * D.lq * D.d), kv = align_up(D.esz * D.b * D.hkv * D.lk * D.d);
-  return 2 * q + 2 * kv + ba_attention_workspace_size(prob, params);
+  const HostPlan h = plan_host(D, prob, params);
+  return 2 * align_up(h.q_bytes) + 2 * align_up(h.kv_bytes) + h.ws_chunk;
 }
 
 ba_status ba_attention_host(const ba_problem *prob, const ba_params *params, const void *q_host,
@@ -406,22 +467,60 @@ ba_status ba_attention_host(const ba_problem *prob, const ba_params *params, con
   if (!workspace) return fail(BA_ERR_INVALID_ARGUMENT, "workspace is NULL");
   const size_t need = ba_attention_host_workspace_size(prob, params);
   if (workspace_bytes < need) return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu < %zu", workspace_bytes, need);
-  const size_t qb = D.esz * D.b * D.hq * D.lq * D.d, kvb = D.esz * D.b * D.hkv * D.lk * D.d;
+  const HostPlan hp = plan_host(D, prob, params);
   char *w = static_cast<char *>(workspace);
-  void *qd = w; w += align_up(qb);
-  void *kd = w; w += align_up(kvb);
-  void *vd = w; w += align_up(kvb);
-  void *od = w; w += align_up(qb);
-  BA_TRY(cuda_check(cudaMemcpyAsync(qd, q_host, qb, cudaMemcpyHostToDevice, stream), "H2D q"));
-  BA_TRY(cuda_check(cudaMemcpyAsync(kd, k_host, kvb, cudaMemcpyHostToDevice, stream), "H2D k"));
-  BA_TRY(cuda_check(cudaMemcpyAsync(vd, v_host, kvb, cudaMemcpyHostToDevice, stream), "H2D v"));
-  ba_problem p = *prob;
-  p.q_stride[2] = D.d; p.q_stride[1] = D.lq * D.d; p.q_stride[0] = D.hq * D.lq * D.d;
-  p.o_stride[0] = p.q_stride[0]; p.o_stride[1] = p.q_stride[1]; p.o_stride[2] = p.q_stride[2];
-  p.k_stride[2] = D.d; p.k_stride[1] = D.lk * D.d; p.k_stride[0] = D.hkv * D.lk * D.d;
-  for (int i = 0; i < 3; ++i) p.v_stride[i] = p.k_stride[i];
-  BA_TRY(ba_attention(&p, params, qd, kd, vd, od, nullptr, w, workspace_bytes - (size_t)(w - static_cast<char *>(workspace)), stream));
-  BA_TRY(cuda_check(cudaMemcpyAsync(out_host, od, qb, cudaMemcpyDeviceToHost, stream), "D2H out"));
+  char *qd = w; w += align_up(hp.q_bytes);
+  char *kd = w; w += align_up(hp.kv_bytes);
+  char *vd = w; w += align_up(hp.kv_bytes);
+  char *od = w; w += align_up(hp.q_bytes);
+  void *ws_chunk = w;
+  cudaStream_t h2d, d2h;
+  BA_TRY(cuda_check(copy_streams(&h2d, &d2h), "copy streams"));
+  const int64_t grp = D.hq / D.hkv;
+  const int64_t n_chunks = D.b * hp.chunks_per_batch;
+  // events: start (caller's prior work), per chunk: inputs landed, compute done, output landed
+  std::vector<cudaEvent_t> ev(3 * n_chunks + 1);
+  for (auto &e : ev) BA_TRY(cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"));
+  struct Guard {
+    std::vector<cudaEvent_t> &v;
+    ~Guard() { for (auto e : v) cudaEventDestroy(e); }  // released once the recorded work completes
+  } guard{ev};
+  BA_TRY(cuda_check(cudaEventRecord(ev[0], stream), "record"));
+  BA_TRY(cuda_check(cudaStreamWaitEvent(h2d, ev[0], 0), "wait"));
+  BA_TRY(cuda_check(cudaStreamWaitEvent(d2h, ev[0], 0), "wait"));
+  struct Span { int64_t q_off, kv_off, nkv; };
+  auto span = [&](int64_t c) {
+    const int64_t b = c / hp.chunks_per_batch, k0 = (c % hp.chunks_per_batch) * hp.kv_per_chunk;
+    const int64_t nkv = std::min<int64_t>(hp.kv_per_chunk, D.hkv - k0);
+    return Span{(b * D.hq + k0 * grp) * D.lq * D.d * (int64_t)D.esz, (b * D.hkv + k0) * D.lk * D.d * (int64_t)D.esz, nkv};
+  };
+  for (int64_t c = 0; c < n_chunks; ++c) {  // all inputs, in chunk order, on the H2D stream
+    const Span sp = span(c);
+    const size_t qb = sp.nkv * grp * D.lq * D.d * D.esz, kb = sp.nkv * D.lk * D.d * D.esz;
+    BA_TRY(cuda_check(cudaMemcpyAsync(qd + sp.q_off, static_cast<const char *>(q_host) + sp.q_off, qb, cudaMemcpyHostToDevice, h2d), "H2D q"));
+    BA_TRY(cuda_check(cudaMemcpyAsync(kd + sp.kv_off, static_cast<const char *>(k_host) + sp.kv_off, kb, cudaMemcpyHostToDevice, h2d), "H2D k"));
+    BA_TRY(cuda_check(cudaMemcpyAsync(vd + sp.kv_off, static_cast<const char *>(v_host) + sp.kv_off, kb, cudaMemcpyHostToDevice, h2d), "H2D v"));
+    BA_TRY(cuda_check(cudaEventRecord(ev[1 + 3 * c], h2d), "record"));
+  }
+  int launches = 0;
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const Span sp = span(c);
+    ba_problem cp = hp.chunk_prob;
+    cp.heads_kv = (int32_t)sp.nkv;
+    cp.heads_q = (int32_t)(sp.nkv * grp);
+    BA_TRY(cuda_check(cudaStreamWaitEvent(stream, ev[1 + 3 * c], 0), "wait"));
+    BA_TRY(ba_attention(&cp, params, qd + sp.q_off, kd + sp.kv_off, vd + sp.kv_off, od + sp.q_off, nullptr, ws_chunk,
+                        hp.ws_chunk, stream));
+    launches += g_launches;
+    BA_TRY(cuda_check(cudaEventRecord(ev[2 + 3 * c], stream), "record"));
+    BA_TRY(cuda_check(cudaStreamWaitEvent(d2h, ev[2 + 3 * c], 0), "wait"));
+    const size_t qb = sp.nkv * grp * D.lq * D.d * D.esz;
+    BA_TRY(cuda_check(cudaMemcpyAsync(static_cast<char *>(out_host) + sp.q_off, od + sp.q_off, qb, cudaMemcpyDeviceToHost, d2h), "D2H out"));
+    BA_TRY(cuda_check(cudaEventRecord(ev[3 + 3 * c], d2h), "record"));
+  }
+  // the caller's stream completes only after the last output byte landed
+  BA_TRY(cuda_check(cudaStreamWaitEvent(stream, ev[3 * n_chunks], 0), "wait"));
+  g_launches = launches;
   return BA_OK;
 }
 

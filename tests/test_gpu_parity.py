@@ -179,9 +179,12 @@ def test_injected_oracle_mask(ba):
     assert ref_sel  # oracle selection computed on the same inputs
 
 
-def test_end_to_end_host_api(ba):
-    w = CONFIGS["A"]
-    q, k, v = make_qkv(w, device="cpu", seq_len=1024, heads_q=2, heads_kv=2)
+@pytest.mark.parametrize("cfg,L,hq,hkv,b", [("A", 1024, 2, 2, 1), ("C", 2048 + 64, 8, 2, 2), ("A", 1000, 16, 16, 1)])
+def test_end_to_end_host_api(ba, cfg, L, hq, hkv, b):
+    """ba_attention_host (chunked over KV heads, copies overlapped with compute)
+    is bit-identical to ba_attention on device-resident inputs."""
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cpu", seq_len=L, heads_q=hq, heads_kv=hkv, batch=b)
     qh, kh, vh = q.pin_memory(), k.pin_memory(), v.pin_memory()
     oh = torch.empty_like(qh).pin_memory()
     ws = torch.empty(ba.attention_host_workspace_size(qh, kh, vh), dtype=torch.uint8, device="cuda")
