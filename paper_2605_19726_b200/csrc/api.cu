@@ -3,6 +3,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
@@ -262,13 +263,26 @@ AttnArgs make_attn(const Dims &D, const ba_params *pa) {
   return a;
 }
 
+// B = 128 runs the 2-CTA cluster kernel (query-block pairs share K/V tiles);
+// BA_ATTN_1CTA=1 selects the single-CTA kernel instead (A/B comparisons).
+bool use_2cta(const AttnArgs &a) {
+  static int one_cta = -1;
+  if (one_cta < 0) {
+    const char *env = getenv("BA_ATTN_1CTA");
+    one_cta = env && atoi(env) ? 1 : 0;
+  }
+  return !one_cta && attn_2cta_supported(a);
+}
+
 const char *attn_kernel_name(const AttnArgs &a) {
+  if (use_2cta(a)) return "attn_sm100_tcgen05_2cta";
   return attn_sm100_supported(a) ? "attn_sm100_tcgen05" : "attn_simt";
 }
 
 ba_status run_attn(const AttnArgs &a, cudaStream_t st) {
   cudaError_t e;
-  if (attn_sm100_supported(a)) e = launch_attn_sm100(a, st);
+  if (use_2cta(a)) e = launch_attn_2cta(a, st);
+  else if (attn_sm100_supported(a)) e = launch_attn_sm100(a, st);
   else e = launch_attn_simt(a, st);
   g_launches = 1;
   return cuda_check(e, attn_kernel_name(a));

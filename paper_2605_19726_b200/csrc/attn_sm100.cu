@@ -41,6 +41,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "sm100_ptx.cuh"
 
 namespace baatt {
 namespace sm100 {
@@ -86,146 +87,11 @@ struct __align__(8) BarsT {
   uint64_t v_full[NVS], v_empty[NVS];
   uint64_t s_full[2], p_full[2];
   uint64_t o_done;
+  uint64_t o_final;  // single phase: every PV of the tile has completed (epilogue)
   uint32_t tmem_base;
   uint32_t n_union;
   uint32_t last_ragged;
 };
-
-// ------------------------------------------------------------------ PTX wrappers
-BA_DEVICE uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-
-BA_DEVICE void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-BA_DEVICE void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-BA_DEVICE void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-BA_DEVICE void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-BA_DEVICE void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-BA_DEVICE void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-BA_DEVICE void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-BA_DEVICE void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-BA_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-BA_DEVICE void named_bar_sync(int id, int count) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory"); }
-
-
-BA_DEVICE void tma_prefetch(const CUtensorMap *m) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
-}
-BA_DEVICE void tma_load_4d(uint32_t dst, const CUtensorMap *m, uint64_t *bar, int c0, int c1, int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
-      : "memory");
-}
-
-BA_DEVICE void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc));
-}
-BA_DEVICE void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc));
-}
-BA_DEVICE void mma_commit(uint64_t *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-#include "tmem_ldst.inc"
-
-BA_DEVICE float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-BA_DEVICE float fmax3(float a, float b, float c) {
-  float d;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
-// Packed fp32x2 ops (FFMA2 / FADD2 on sm_100): half the issue slots of scalar fp32.
-BA_DEVICE uint64_t f2(float lo, float hi) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-BA_DEVICE void unf2(uint64_t v, float &lo, float &hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
-BA_DEVICE uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-BA_DEVICE uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-// 2^x for a pair on the FMA/ALU pipes (offloads the MUFU, FA4-style):
-// x = xi + f with xi = rint(x) via the 1.5*2^23 trick, 2^f by a degree-3
-// minimax polynomial on [-1/2, 1/2] (max rel. error 2.3e-4, below bf16's
-// 2^-9), 2^xi added into the exponent bits.  Inputs are clamped to >= -126.
-BA_DEVICE uint64_t exp2_poly2(uint64_t x2) {
-  float x0, x1;
-  unf2(x2, x0, x1);
-  x2 = f2(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
-  const uint64_t magic = f2(12582912.f, 12582912.f);
-  const uint64_t t = fadd2(x2, magic);
-  const uint64_t xi = fadd2(t, f2(-12582912.f, -12582912.f));
-  const uint64_t fr = ffma2(xi, f2(-1.f, -1.f), x2);
-  uint64_t p = ffma2(f2(0.0554986224f, 0.0554986224f), fr, f2(0.243548840f, 0.243548840f));
-  p = ffma2(p, fr, f2(0.693232119f, 0.693232119f));
-  p = ffma2(p, fr, f2(0.999772966f, 0.999772966f));
-  float p0, p1, t0, t1;
-  unf2(p, p0, p1);
-  unf2(t, t0, t1);
-  const float r0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
-  const float r1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
-  return f2(r0, r1);
-}
-BA_DEVICE uint32_t pack_bf16(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
-
-// UMMA shared-memory descriptor (sm_100, version 1), 128-byte swizzle.
-// K-major tiles: SBO = 1024 B between 8-row groups, LBO unused (1).
-// MN-major tiles: LBO = byte distance between 64-element swizzle atoms along
-// MN, SBO = 1024 B between 8-row groups along K.
-BA_DEVICE uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= 1ull << 46;                // version (sm_100)
-  d |= 2ull << 61;                // SWIZZLE_128B
-  return d;
-}
-
 
 // Ordered walk over the set bits of (A | B).
 struct UnionWalk {
@@ -316,6 +182,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
     for (int s = 0; s < C::NVS; ++s) { mbar_init(&bars.v_full[s], 1); mbar_init(&bars.v_empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&bars.s_full[s], 1); mbar_init(&bars.p_full[s], 8); }
     mbar_init(&bars.o_done, 1);
+    mbar_init(&bars.o_final, 1);
     fence_barrier_init();
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
@@ -393,6 +260,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
         mma_commit(&bars.v_empty[s]);
         mma_commit(&bars.o_done);
       }
+      mma_commit(&bars.o_final);
     }
     __syncwarp();
   } else if (warp >= kSoftmaxWarp0 && warp < kSoftmaxWarp0 + 8) {
@@ -538,7 +406,9 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
     named_bar_sync(1 + qd, 64);
     const float lt = l + red2[(hf ^ 1) * 128 + r];
     if (cnt > 0) {
-      mbar_wait(&bars.o_done, (uint32_t)(cnt - 1) & 1u);
+      // not o_done: when this tile's softmax skipped its last tiles it can arrive here with
+      // only cnt-2 PVs complete, which the parity of o_done cannot tell from cnt
+      mbar_wait(&bars.o_final, 0);
       tc_fence_after();
     }
     const float inv = lt > 0.f ? 1.f / lt : 0.f;

@@ -74,5 +74,7 @@ struct AttnArgs {
 cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t st);
 cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st);
 bool attn_sm100_supported(const AttnArgs &a);
+cudaError_t launch_attn_2cta(const AttnArgs &a, cudaStream_t st);
+bool attn_2cta_supported(const AttnArgs &a);
 
 }  // namespace baatt

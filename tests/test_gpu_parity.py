@@ -179,6 +179,42 @@ def test_injected_oracle_mask(ba):
     assert ref_sel  # oracle selection computed on the same inputs
 
 
+@pytest.mark.parametrize("B,one_cta", [(128, False), (128, True), (64, False)])
+def test_injected_dissimilar_lists(ba, B, one_cta):
+    """Random (dissimilar) index lists for every query block: exercises the
+    pair kernels' union walk where a block skips tiles (P = 0 rows), including
+    a skipped LAST tile (the epilogue must still wait for every PV)."""
+    import subprocess, sys, os
+    env = dict(os.environ)
+    if one_cta:
+        env["BA_ATTN_1CTA"] = "1"
+    code = f"""
+import sys; sys.path.insert(0, {os.path.join(os.path.dirname(__file__))!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import numpy as np, torch
+import paper_2605_19726_b200.baatt as ba
+from synth import CONFIGS, make_qkv
+from parity import oracle_output_with_gpu_selection, max_abs_err
+B = {B}
+w = CONFIGS["A" if B == 128 else "M"]
+for seed in range(4):
+    q, k, v = make_qkv(w, device="cuda", seq_len=16 * B + 37, heads_q=2, heads_kv=1)
+    ctx = ba.Context(q, k, v, B, 0.5)
+    sel = ctx.select(q, k, v)
+    nk, kap = sel.n_k, sel.kappa
+    rng = np.random.default_rng(seed)
+    idx = np.sort(np.stack([np.stack([rng.choice(nk, kap, replace=False) for _ in range(sel.n_q)]) for _ in range(2)]), axis=-1)
+    sel.kv_index.copy_(torch.from_numpy(idx[None].astype(np.int32)))
+    out = torch.empty_like(q)
+    ctx.sparse_attn(out)
+    torch.cuda.synchronize()
+    err = max_abs_err(out, oracle_output_with_gpu_selection(q, k, v, sel, B))
+    assert err <= 2e-2, (seed, err)
+print("OK", ba.attention_kernel_name(q, k, v, B))
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=240)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("cfg,L,hq,hkv,b", [("A", 1024, 2, 2, 1), ("C", 2048 + 64, 8, 2, 2), ("A", 1000, 16, 16, 1)])
 def test_end_to_end_host_api(ba, cfg, L, hq, hkv, b):
     """ba_attention_host (chunked over KV heads, copies overlapped with compute)
