@@ -263,15 +263,16 @@ AttnArgs make_attn(const Dims &D, const ba_params *pa) {
   return a;
 }
 
-// B = 128 runs the 2-CTA cluster kernel (query-block pairs share K/V tiles);
-// BA_ATTN_1CTA=1 selects the single-CTA kernel instead (A/B comparisons).
+// B = 128 runs the single-CTA kernel; BA_ATTN_2CTA=1 selects the 2-CTA cluster
+// kernel (query-block pairs share K/V tiles) — correct and tested, but slower
+// than the single-CTA kernel in round 1, so opt-in.
 bool use_2cta(const AttnArgs &a) {
-  static int one_cta = -1;
-  if (one_cta < 0) {
-    const char *env = getenv("BA_ATTN_1CTA");
-    one_cta = env && atoi(env) ? 1 : 0;
+  static int two_cta = -1;
+  if (two_cta < 0) {
+    const char *env = getenv("BA_ATTN_2CTA");
+    two_cta = env && atoi(env) ? 1 : 0;
   }
-  return !one_cta && attn_2cta_supported(a);
+  return two_cta && attn_2cta_supported(a);
 }
 
 const char *attn_kernel_name(const AttnArgs &a) {

@@ -158,8 +158,11 @@ BA_DEVICE uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+// arrive on a barrier of another CTA of the cluster (plain form: a cluster-scope
+// release here costs ~1000 cycles per arrive; the data it guards is TMEM,
+// ordered by tcgen05.wait::st + tcgen05.fence::before_thread_sync)
 BA_DEVICE void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 BA_DEVICE void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -180,6 +183,15 @@ BA_DEVICE void mma_ts_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uin
       "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
       "}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc));
+}
+BA_DEVICE void mma_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc));
 }
 // commit the issuing thread's prior tcgen05 ops to the same-offset barrier of every CTA in `mask`
 BA_DEVICE void mma_commit_2sm_mc(uint64_t *bar, uint16_t mask) {

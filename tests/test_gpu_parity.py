@@ -179,15 +179,15 @@ def test_injected_oracle_mask(ba):
     assert ref_sel  # oracle selection computed on the same inputs
 
 
-@pytest.mark.parametrize("B,one_cta", [(128, False), (128, True), (64, False)])
-def test_injected_dissimilar_lists(ba, B, one_cta):
+@pytest.mark.parametrize("B,two_cta", [(128, False), (128, True), (64, False)])
+def test_injected_dissimilar_lists(ba, B, two_cta):
     """Random (dissimilar) index lists for every query block: exercises the
     pair kernels' union walk where a block skips tiles (P = 0 rows), including
     a skipped LAST tile (the epilogue must still wait for every PV)."""
     import subprocess, sys, os
     env = dict(os.environ)
-    if one_cta:
-        env["BA_ATTN_1CTA"] = "1"
+    if two_cta:
+        env["BA_ATTN_2CTA"] = "1"
     code = f"""
 import sys; sys.path.insert(0, {os.path.join(os.path.dirname(__file__))!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
 import numpy as np, torch
@@ -236,3 +236,30 @@ def test_errors_are_loud(ba):
     q, k, v = make_qkv(w, device="cuda", seq_len=256, heads_q=3, heads_kv=2)
     with pytest.raises(ba.BaError, match="SHAPE_MISMATCH"):
         ba.ba_attention(q, k, v)
+
+
+def test_two_cta_kernel_parity(ba):
+    """The opt-in 2-CTA cluster kernel (BA_ATTN_2CTA=1) on real selections,
+    ragged lengths, GQA and an odd number of query blocks."""
+    import os, subprocess, sys
+    env = dict(os.environ, BA_ATTN_2CTA="1")
+    code = f"""
+import sys; sys.path.insert(0, {os.path.dirname(__file__)!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import torch
+import paper_2605_19726_b200.baatt as ba
+from synth import CONFIGS, make_qkv
+from parity import oracle_output_with_gpu_selection, max_abs_err
+for cfg, L, hq, hkv, dens in (("A", 4096 + 77, 2, 2, 0.5), ("C", 3 * 128 * 5, 4, 1, 0.25), ("V", 2 * 128 * 9 + 80, 2, 2, 0.5)):
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv)
+    ctx = ba.Context(q, k, v, 128, dens)
+    sel = ctx.select(q, k, v)
+    out = torch.empty_like(q)
+    ctx.sparse_attn(out)
+    torch.cuda.synchronize()
+    err = max_abs_err(out, oracle_output_with_gpu_selection(q, k, v, sel, 128))
+    assert err <= 2e-2, (cfg, err)
+print("OK", ba.attention_kernel_name(q, k, v, 128))
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=240)
+    assert r.returncode == 0 and "OK attn_sm100_tcgen05_2cta" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

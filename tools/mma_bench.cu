@@ -1,0 +1,93 @@
+// mma_bench.cu — tcgen05 issue/execute rate for the attention kernel's MMA mix,
+// operands resident (no TMA, no softmax): cycles per (S = Q K^T, O += P V) pair.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../paper_2605_19726_b200/csrc/sm100_ptx.cuh"
+using namespace baatt::sm100;
+
+// 0: S TS + PV TS, 1: S SS + PV TS, 2: S SS only, 3: PV TS only,
+// 4: mode 0 + a commit after each 8-MMA group, 5: mode 4 + fence + wait on a completed barrier per group
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) mma_kernel(int iters, long long *out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const uint32_t raw = smem_u32(sm), base = (raw + 1023u) & ~1023u;
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t cbar[4];
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&cbar[i], 1);
+    mbar_init(&cbar[3], 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | (16u << 17) | (8u << 24);
+  const uint32_t IDO = IDS | (1u << 16);
+  long long t0 = 0, t1 = 0;
+  if (threadIdx.x == 0) {
+    const uint32_t sq = base, sk = base + 32768, sv = base + 65536;
+    t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const uint32_t sc = (it % 3) * 128;
+      if (MODE != 3) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          if (MODE == 0 || MODE >= 4) mma_ts(tmem + sc, tmem + 384 + kk * 8, make_desc(sk + off, 16, 1024), IDS, kk > 0);
+          else mma_ss(tmem + sc, make_desc(sq + off, 16, 1024), make_desc(sk + off, 16, 1024), IDS, kk > 0);
+        }
+      }
+      if (MODE != 2) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + 384 - 128 * (MODE == 0 || MODE >= 4), tmem + sc + kk * 8, make_desc(sv + kk * 2048, 16384, 1024), IDO, 1);
+      }
+      if (MODE >= 4) { mma_commit(&cbar[0]); mma_commit(&cbar[1]); }
+      if (MODE == 5) { mbar_wait(&cbar[3], 1); tc_fence_after(); }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+int main() {
+  long long *d, h[148];
+  cudaMalloc(&d, 148 * 8);
+  const int iters = 2000;
+  const char *names[4] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  "};
+  const char *names2[6] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  ", "+commits    ", "+commit+wait"};
+  for (int mode = 0; mode < 6; ++mode) {
+    auto k = mode == 0 ? mma_kernel<0> : mode == 1 ? mma_kernel<1> : mode == 2 ? mma_kernel<2> : mode == 3 ? mma_kernel<3> : mode == 4 ? mma_kernel<4> : mma_kernel<5>;
+    names[mode % 4] = names2[mode];
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int rep = 0; rep < 2; ++rep) {
+      k<<<148, 128, 100 * 1024>>>(iters, d);
+      cudaDeviceSynchronize();
+    }
+    cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
+    double c = 0;
+    for (int i = 0; i < 148; ++i) c += h[i];
+    c /= 148;
+    const int mmas = (mode < 2 || mode >= 4 ? 16 : 8);
+    printf("%s: %.1f cycles per iteration (%d MMAs of 128x128x16) = %.1f cyc/MMA (floor 64)\n", names2[mode], c / iters, mmas, c / iters / mmas);
+  }
+  printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
