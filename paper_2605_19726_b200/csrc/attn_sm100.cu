@@ -206,6 +206,8 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
     uint64_t *full = is_k ? bars.k_full : bars.v_full;
     uint64_t *empty = is_k ? bars.k_empty : bars.v_empty;
     const uint32_t ring = base + (is_k ? C::SMEM_K : C::SMEM_V);
+    // profiling knob (no-softmax variant only): skip_load bit 0 = V, bit 1 = K
+    const bool skip = kNoSoftmax && ((a.dbg_flags >> (is_k ? 1 : 0)) & 1);
     if (lane == 0 && cnt > 0) {
       UnionWalk walk;
       walk.init(mask_a, mask_b);
@@ -215,6 +217,10 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
         const uint32_t ph = (uint32_t)(j / nst) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
         TR(is_k ? 0 : 1, j);
+        if (skip) {
+          mbar_arrive(&full[s]);
+          continue;
+        }
         const uint32_t dst = ring + s * C::TILE_BYTES;
         mbar_expect_tx(&full[s], C::TILE_BYTES);
         tma_load_4d(dst, map, &full[s], 0, gk * kBN, (int)hk, (int)b);
@@ -521,7 +527,12 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
     dbg = d ? atoi(d) : 0;
   }
   if (a.B == 64) return launch_variant<64, 0, false, false>(a, mk, mv, st);
-  if (dbg == 1) return launch_variant<128, 0, true, false>(a, mk, mv, st);
+  if (dbg == 1) {
+    AttnArgs b2 = a;
+    const char *sk = getenv("BA_ATTN_SKIPLOAD");
+    b2.dbg_flags = sk ? atoi(sk) : 0;
+    return launch_variant<128, 0, true, false>(b2, mk, mv, st);
+  }
   if (dbg == 2) return launch_variant<128, 0, false, true>(a, mk, mv, st);
   switch (emu) {
     case 1: return launch_variant<128, 1, false, false>(a, mk, mv, st);

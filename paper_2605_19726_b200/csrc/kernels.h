@@ -70,6 +70,7 @@ struct AttnArgs {
   int64_t os[3];
   float *lse;                  // [b, hq, lq] or nullptr
   float scale;
+  int dbg_flags;               // profiling-only knobs (0 in normal use)
 };
 cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t st);
 cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st);

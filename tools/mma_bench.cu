@@ -8,13 +8,15 @@ using namespace baatt::sm100;
 
 // 0: S TS + PV TS, 1: S SS + PV TS, 2: S SS only, 3: PV TS only,
 // 4: mode 0 + a commit after each 8-MMA group, 5: mode 4 + fence + wait on a completed barrier per group
+// 6: the kernel's handoff: S_{j+1} issued, then wait for warp 1 to see S_j complete and arrive, then PV_j
 template <int MODE>
-__global__ void __launch_bounds__(128, 1) mma_kernel(int iters, long long *out) {
+__global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const uint32_t raw = smem_u32(sm), base = (raw + 1023u) & ~1023u;
   __shared__ uint32_t tslot;
   __shared__ __align__(8) uint64_t bar;
   __shared__ __align__(8) uint64_t cbar[4];
+  __shared__ __align__(8) uint64_t sfull[2], pfull[2];
   const int warp = threadIdx.x >> 5;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
@@ -24,6 +26,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, long long *out) 
     mbar_init(&bar, 1);
     for (int i = 0; i < 4; ++i) mbar_init(&cbar[i], 1);
     mbar_init(&cbar[3], 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&pfull[i], MODE == 7 ? 8 : 1); }
     fence_barrier_init();
   }
   tc_fence_before();
@@ -33,7 +36,42 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, long long *out) 
   const uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | (16u << 17) | (8u << 24);
   const uint32_t IDO = IDS | (1u << 16);
   long long t0 = 0, t1 = 0;
-  if (threadIdx.x == 0) {
+  if (MODE == 6 || MODE == 7) {
+    if (threadIdx.x == 0) {
+      const uint32_t sk = base + 32768, sv = base + 65536;
+      auto issue_s = [&](int j) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ts(tmem + (j & 1) * 128, tmem + 384 + kk * 8, make_desc(sk + off, 16, 1024), IDS, kk > 0);
+        }
+        mma_commit(&sfull[j & 1]);
+      };
+      t0 = clock64();
+      issue_s(0);
+      for (int j = 0; j < iters; ++j) {
+        if (j + 1 < iters) issue_s(j + 1);
+        mbar_wait(&pfull[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + 256, tmem + (j & 1) * 128 + kk * 8, make_desc(sv + kk * 2048, 16384, 1024), IDO, 1);
+      }
+      mma_commit(&bar);
+      mbar_wait(&bar, 0);
+      t1 = clock64();
+      out[blockIdx.x] = t1 - t0;
+    } else if ((MODE == 6 && threadIdx.x == 32) || (MODE == 7 && threadIdx.x >= 64 && threadIdx.x < 320)) {
+      // MODE 7: 8 warps (256 threads) wait like the softmax warpgroups, one elected arrive per warp
+      for (int j = 0; j < iters; ++j) {
+        mbar_wait(&sfull[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        tc_fence_before();
+        if (MODE == 7) __syncwarp();
+        if (MODE == 6 || (threadIdx.x & 31) == 0) mbar_arrive(&pfull[j & 1]);
+      }
+    }
+  } else if (threadIdx.x == 0) {
     const uint32_t sq = base, sk = base + 32768, sv = base + 65536;
     t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -72,20 +110,20 @@ int main() {
   cudaMalloc(&d, 148 * 8);
   const int iters = 2000;
   const char *names[4] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  "};
-  const char *names2[6] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  ", "+commits    ", "+commit+wait"};
-  for (int mode = 0; mode < 6; ++mode) {
-    auto k = mode == 0 ? mma_kernel<0> : mode == 1 ? mma_kernel<1> : mode == 2 ? mma_kernel<2> : mode == 3 ? mma_kernel<3> : mode == 4 ? mma_kernel<4> : mma_kernel<5>;
-    names[mode % 4] = names2[mode];
+  const char *names2[8] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  ", "+commits    ", "+commit+wait", "handoff     ", "handoff x8w "};
+  for (int mode = 0; mode < 8; ++mode) {
+    auto k = mode == 0 ? mma_kernel<0> : mode == 1 ? mma_kernel<1> : mode == 2 ? mma_kernel<2> : mode == 3 ? mma_kernel<3> : mode == 4 ? mma_kernel<4> : mode == 5 ? mma_kernel<5> : mode == 6 ? mma_kernel<6> : mma_kernel<7>;
+
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     for (int rep = 0; rep < 2; ++rep) {
-      k<<<148, 128, 100 * 1024>>>(iters, d);
+      k<<<148, 352, 100 * 1024>>>(iters, d);
       cudaDeviceSynchronize();
     }
     cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
     double c = 0;
     for (int i = 0; i < 148; ++i) c += h[i];
     c /= 148;
-    const int mmas = (mode < 2 || mode >= 4 ? 16 : 8);
+    const int mmas = (mode < 2 || mode >= 4 ? 16 : 8);  // mode 6: S + PV per iteration
     printf("%s: %.1f cycles per iteration (%d MMAs of 128x128x16) = %.1f cyc/MMA (floor 64)\n", names2[mode], c / iters, mmas, c / iters / mmas);
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
