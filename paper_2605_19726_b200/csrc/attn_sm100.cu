@@ -15,9 +15,10 @@
 //            block get P = 0.  (tcgen05 M = 128 at half the rows would waste
 //            half the tensor pipe; the pair recovers it where lists overlap.)
 // 11 warps:
-//   warps 0,10 TMA producers: K_u (warp 0) and V_u (warp 10) of the u-th key
-//              block of the (union) list into independent rings (128-byte
-//              swizzle, two 64-column boxes per tile).
+//   warp 0     TMA producer: K_u and V_u of the u-th key block of the (union)
+//              list into one stage of a 3-stage ring (128-byte swizzle, two
+//              64-column boxes per tile): one "full" wait per tile for the
+//              MMA issuer.  (warp 10 is idle.)
 //   warp 1     MMA issuer (one elected thread) and TMEM owner.  S_u = Q K_u^T
 //              with Q held in TMEM (TS form: smem carries only K and V), into
 //              a double-buffered TMEM accumulator, then O += P_u V_u with P_u
@@ -61,8 +62,10 @@ template <int kBN>
 struct Cfg {
   static constexpr uint32_t BOX_BYTES = kBN * 64 * 2;      // kBN rows x 64 bf16 columns
   static constexpr uint32_t TILE_BYTES = 2 * BOX_BYTES;    // kBN x 128
-  static constexpr int NKS = 4 * (128 / kBN);              // K stages (same bytes for both B)
-  static constexpr int NVS = 2 * (128 / kBN);              // V stages (V is consumed a tile after K)
+  // one ring of (K, V) stages: a single "full" wait per tile in the MMA thread
+  // (each blocking mbarrier wait costs the lone MMA issuer ~100 cycles that
+  // the shallow tcgen05 queue cannot hide — tools/mma_bench.cu modes 8/9)
+  static constexpr int NKV = 3 * (128 / kBN);
   static constexpr int HC = kBN / 2;                       // S columns per softmax half
   static constexpr bool kPair = kBN == 64;
   // instruction descriptors, kind::f16: D fp32, A/B bf16, dense, M = 128
@@ -70,9 +73,8 @@ struct Cfg {
                                       ((uint32_t)(BM >> 4) << 24);                    // A K-major (Q), B K-major (K)
   static constexpr uint32_t IDESC_O = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(HD >> 3) << 17) |
                                       ((uint32_t)(BM >> 4) << 24) | (1u << 16);       // B MN-major (V: d contiguous)
-  static constexpr uint32_t SMEM_K = 0;
-  static constexpr uint32_t SMEM_V = SMEM_K + NKS * TILE_BYTES;
-  static constexpr uint32_t SMEM_RED = SMEM_V + NVS * TILE_BYTES;     // float [2][2][128] row-max exchange
+  static constexpr uint32_t SMEM_KV = 0;                              // stage s: K at +0, V at +TILE_BYTES
+  static constexpr uint32_t SMEM_RED = SMEM_KV + NKV * 2 * TILE_BYTES;  // float [2][2][128] row-max exchange
   static constexpr uint32_t SMEM_RED2 = SMEM_RED + 2 * 2 * 128 * 4;   // float [2][128] final l exchange
   static constexpr uint32_t SMEM_MASK = SMEM_RED2 + 2 * 128 * 4;      // uint32 [2][kMaskWords]
   static constexpr uint32_t SMEM_BARS = SMEM_MASK + 2 * kMaskWords * 4;
@@ -80,11 +82,10 @@ struct Cfg {
   static __device__ constexpr uint32_t s_col(int buf) { return buf ? (uint32_t)kBN : 0u; }
 };
 
-template <int NKS, int NVS>
+template <int NKV>
 struct __align__(8) BarsT {
   uint64_t q_full;
-  uint64_t k_full[NKS], k_empty[NKS];
-  uint64_t v_full[NVS], v_empty[NVS];
+  uint64_t kv_full[NKV], kv_empty[NKV];
   uint64_t s_full[2], p_full[2];
   uint64_t o_done;
   uint64_t o_final;  // single phase: every PV of the tile has completed (epilogue)
@@ -118,7 +119,7 @@ template <int kBN, int kEmu, bool kNoSoftmax = false, bool kTrace = false>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
   using C = Cfg<kBN>;
-  using Bars = BarsT<C::NKS, C::NVS>;
+  using Bars = BarsT<C::NKV>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -178,8 +179,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
 
   if (warp == 0 && lane == 0) {
     mbar_init(&bars.q_full, 8);   // one elected arrive per softmax warp
-    for (int s = 0; s < C::NKS; ++s) { mbar_init(&bars.k_full[s], 1); mbar_init(&bars.k_empty[s], 1); }
-    for (int s = 0; s < C::NVS; ++s) { mbar_init(&bars.v_full[s], 1); mbar_init(&bars.v_empty[s], 1); }
+    for (int s = 0; s < C::NKV; ++s) { mbar_init(&bars.kv_full[s], 1); mbar_init(&bars.kv_empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&bars.s_full[s], 1); mbar_init(&bars.p_full[s], 8); }
     mbar_init(&bars.o_done, 1);
     mbar_init(&bars.o_final, 1);
@@ -196,35 +196,29 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
 
-  if (warp == 0 || warp == kVProducerWarp) {
-    // ================================================================ TMA producers
-    // warp 0 streams K_u, the last warp streams V_u: independent rings, so a
-    // wait for a free V slot never delays the next K load (and vice versa).
-    const bool is_k = warp == 0;
-    const int nst = is_k ? C::NKS : C::NVS;
-    const CUtensorMap *map = is_k ? &tm_k : &tm_v;
-    uint64_t *full = is_k ? bars.k_full : bars.v_full;
-    uint64_t *empty = is_k ? bars.k_empty : bars.v_empty;
-    const uint32_t ring = base + (is_k ? C::SMEM_K : C::SMEM_V);
-    // profiling knob (no-softmax variant only): skip_load bit 0 = V, bit 1 = K
-    const bool skip = kNoSoftmax && ((a.dbg_flags >> (is_k ? 1 : 0)) & 1);
+  if (warp == 0) {
+    // ================================================================ TMA producer
+    // K_u and V_u of the u-th selected key block into one stage of the ring
+    const bool skip = kNoSoftmax && (a.dbg_flags & 3) == 3;  // profiling knob (no-softmax variant only)
     if (lane == 0 && cnt > 0) {
       UnionWalk walk;
       walk.init(mask_a, mask_b);
       for (int j = 0; j < cnt; ++j) {
         const int gk = walk.next();
-        const int s = j % nst;
-        const uint32_t ph = (uint32_t)(j / nst) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        TR(is_k ? 0 : 1, j);
+        const int s = j % C::NKV;
+        const uint32_t ph = (uint32_t)(j / C::NKV) & 1u;
+        mbar_wait(&bars.kv_empty[s], ph ^ 1u);
+        TR(0, j);
         if (skip) {
-          mbar_arrive(&full[s]);
+          mbar_arrive(&bars.kv_full[s]);
           continue;
         }
-        const uint32_t dst = ring + s * C::TILE_BYTES;
-        mbar_expect_tx(&full[s], C::TILE_BYTES);
-        tma_load_4d(dst, map, &full[s], 0, gk * kBN, (int)hk, (int)b);
-        tma_load_4d(dst + C::BOX_BYTES, map, &full[s], 64, gk * kBN, (int)hk, (int)b);
+        const uint32_t dk = base + C::SMEM_KV + s * 2 * C::TILE_BYTES, dv = dk + C::TILE_BYTES;
+        mbar_expect_tx(&bars.kv_full[s], 2 * C::TILE_BYTES);
+        tma_load_4d(dk, &tm_k, &bars.kv_full[s], 0, gk * kBN, (int)hk, (int)b);
+        tma_load_4d(dk + C::BOX_BYTES, &tm_k, &bars.kv_full[s], 64, gk * kBN, (int)hk, (int)b);
+        tma_load_4d(dv, &tm_v, &bars.kv_full[s], 0, gk * kBN, (int)hk, (int)b);
+        tma_load_4d(dv + C::BOX_BYTES, &tm_v, &bars.kv_full[s], 64, gk * kBN, (int)hk, (int)b);
       }
     }
     __syncwarp();
@@ -234,18 +228,17 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       mbar_wait(&bars.q_full, 0);
       tc_fence_after();
       auto issue_s = [&](int j) {
-        const int s = j % C::NKS;
-        mbar_wait(&bars.k_full[s], (uint32_t)(j / C::NKS) & 1u);
+        const int s = j % C::NKV;
+        mbar_wait(&bars.kv_full[s], (uint32_t)(j / C::NKV) & 1u);  // K_j and V_j landed
         TR(2, j);
         tc_fence_after();
-        const uint32_t sk = base + C::SMEM_K + s * C::TILE_BYTES;
+        const uint32_t sk = base + C::SMEM_KV + s * 2 * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * C::BOX_BYTES + (kk & 3) * 32;
           mma_ts(tmem + C::s_col(j & 1), tmem + Q_COL + kk * 8, make_desc(sk + off, 16, 1024), C::IDESC_S,
                  kk > 0 ? 1u : 0u);
         }
-        mma_commit(&bars.k_empty[s]);
         mma_commit(&bars.s_full[j & 1]);
       };
       issue_s(0);
@@ -253,17 +246,16 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
         if (j + 1 < cnt) issue_s(j + 1);
         mbar_wait(&bars.p_full[j & 1], (uint32_t)(j >> 1) & 1u);
         TR(3, j);
-        const int s = j % C::NVS;
-        mbar_wait(&bars.v_full[s], (uint32_t)(j / C::NVS) & 1u);
+        const int s = j % C::NKV;  // V_j arrived with K_j (waited in issue_s(j))
         TR(4, j);
         tc_fence_after();
-        const uint32_t sv = base + C::SMEM_V + s * C::TILE_BYTES;
+        const uint32_t sv = base + C::SMEM_KV + s * 2 * C::TILE_BYTES + C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
           mma_ts(tmem + O_COL, tmem + C::s_col(j & 1) + kk * 8, make_desc(sv + kk * 2048, C::BOX_BYTES, 1024),
                  C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        mma_commit(&bars.v_empty[s]);
+        mma_commit(&bars.kv_empty[s]);  // stage free once PV_j (the last reader of K_j / V_j) completes
         mma_commit(&bars.o_done);
       }
       mma_commit(&bars.o_final);

@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) 
   __shared__ __align__(8) uint64_t bar;
   __shared__ __align__(8) uint64_t cbar[4];
   __shared__ __align__(8) uint64_t sfull[2], pfull[2];
+  __shared__ __align__(8) uint64_t kfull[4], kempty[4], vfull[2], vempty[2], odone;
   const int warp = threadIdx.x >> 5;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
@@ -26,7 +27,10 @@ __global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) 
     mbar_init(&bar, 1);
     for (int i = 0; i < 4; ++i) mbar_init(&cbar[i], 1);
     mbar_init(&cbar[3], 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&pfull[i], MODE == 7 ? 8 : 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&pfull[i], MODE >= 7 ? 8 : 1); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&kfull[i], 1); mbar_init(&kempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&vfull[i], 1); mbar_init(&vempty[i], 1); }
+    mbar_init(&odone, 1);
     fence_barrier_init();
   }
   tc_fence_before();
@@ -36,15 +40,17 @@ __global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) 
   const uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | (16u << 17) | (8u << 24);
   const uint32_t IDO = IDS | (1u << 16);
   long long t0 = 0, t1 = 0;
-  if (MODE == 6 || MODE == 7) {
+  if (MODE >= 6) {
     if (threadIdx.x == 0) {
       const uint32_t sk = base + 32768, sv = base + 65536;
       auto issue_s = [&](int j) {
+        if (MODE >= 8 && !(MODE == 10 && j >= 2)) { mbar_wait(&kfull[j & 3], (j >> 2) & 1); tc_fence_after(); }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
           mma_ts(tmem + (j & 1) * 128, tmem + 384 + kk * 8, make_desc(sk + off, 16, 1024), IDS, kk > 0);
         }
+        if (MODE == 8) mma_commit(&kempty[j & 3]);
         mma_commit(&sfull[j & 1]);
       };
       t0 = clock64();
@@ -52,22 +58,36 @@ __global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) 
       for (int j = 0; j < iters; ++j) {
         if (j + 1 < iters) issue_s(j + 1);
         mbar_wait(&pfull[j & 1], (j >> 1) & 1);
+        if (MODE == 8) mbar_wait(&vfull[j & 1], (j >> 1) & 1);  // MODE 9: V arrived with K (kfull)
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
+        for (int kk = 0; kk < 8; ++kk) {
+          if (MODE == 10 && kk == 4 && j + 2 < iters) { mbar_wait(&kfull[(j + 2) & 3], ((j + 2) >> 2) & 1); tc_fence_after(); }
           mma_ts(tmem + 256, tmem + (j & 1) * 128 + kk * 8, make_desc(sv + kk * 2048, 16384, 1024), IDO, 1);
+        }
+        if (MODE == 8) { mma_commit(&vempty[j & 1]); mma_commit(&odone); }
+        if (MODE >= 9) { mma_commit(&kempty[j & 3]); mma_commit(&odone); }
       }
       mma_commit(&bar);
       mbar_wait(&bar, 0);
       t1 = clock64();
       out[blockIdx.x] = t1 - t0;
-    } else if ((MODE == 6 && threadIdx.x == 32) || (MODE == 7 && threadIdx.x >= 64 && threadIdx.x < 320)) {
+    } else if (MODE >= 9 && threadIdx.x == 320) {
+      for (int j = 0; j < iters; ++j) { mbar_wait(&kempty[j & 3], ((j >> 2) & 1) ^ 1); mbar_arrive(&kfull[j & 3]); }
+    } else if (MODE == 8 && (threadIdx.x == 320 || threadIdx.x == 32)) {
+      // producers without data: wait for the free slot, arrive on the full barrier (K: 4 stages, V: 2)
+      const bool is_k = threadIdx.x == 320;
+      for (int j = 0; j < iters; ++j) {
+        if (is_k) { mbar_wait(&kempty[j & 3], ((j >> 2) & 1) ^ 1); mbar_arrive(&kfull[j & 3]); }
+        else { mbar_wait(&vempty[j & 1], ((j >> 1) & 1) ^ 1); mbar_arrive(&vfull[j & 1]); }
+      }
+    } else if ((MODE == 6 && threadIdx.x == 32) || (MODE >= 7 && threadIdx.x >= 64 && threadIdx.x < 320)) {
       // MODE 7: 8 warps (256 threads) wait like the softmax warpgroups, one elected arrive per warp
       for (int j = 0; j < iters; ++j) {
         mbar_wait(&sfull[j & 1], (j >> 1) & 1);
         tc_fence_after();
         tc_fence_before();
-        if (MODE == 7) __syncwarp();
+        if (MODE >= 7) __syncwarp();
         if (MODE == 6 || (threadIdx.x & 31) == 0) mbar_arrive(&pfull[j & 1]);
       }
     }
@@ -110,9 +130,9 @@ int main() {
   cudaMalloc(&d, 148 * 8);
   const int iters = 2000;
   const char *names[4] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  "};
-  const char *names2[8] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  ", "+commits    ", "+commit+wait", "handoff     ", "handoff x8w "};
-  for (int mode = 0; mode < 8; ++mode) {
-    auto k = mode == 0 ? mma_kernel<0> : mode == 1 ? mma_kernel<1> : mode == 2 ? mma_kernel<2> : mode == 3 ? mma_kernel<3> : mode == 4 ? mma_kernel<4> : mode == 5 ? mma_kernel<5> : mode == 6 ? mma_kernel<6> : mma_kernel<7>;
+  const char *names2[11] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  ", "+commits    ", "+commit+wait", "handoff     ", "handoff x8w ", "+producers  ", "+1 kv ring  ", "kv wait mid "};
+  for (int mode = 0; mode < 11; ++mode) {
+    auto k = mode == 0 ? mma_kernel<0> : mode == 1 ? mma_kernel<1> : mode == 2 ? mma_kernel<2> : mode == 3 ? mma_kernel<3> : mode == 4 ? mma_kernel<4> : mode == 5 ? mma_kernel<5> : mode == 6 ? mma_kernel<6> : mode == 7 ? mma_kernel<7> : mode == 8 ? mma_kernel<8> : mode == 9 ? mma_kernel<9> : mma_kernel<10>;
 
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     for (int rep = 0; rep < 2; ++rep) {
