@@ -4,6 +4,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <mutex>
@@ -263,26 +264,38 @@ AttnArgs make_attn(const Dims &D, const ba_params *pa) {
   return a;
 }
 
-// B = 128 runs the single-CTA kernel; BA_ATTN_2CTA=1 selects the 2-CTA cluster
-// kernel (query-block pairs share K/V tiles) — correct and tested, but slower
-// than the single-CTA kernel in round 1, so opt-in.
-bool use_2cta(const AttnArgs &a) {
-  static int two_cta = -1;
-  if (two_cta < 0) {
-    const char *env = getenv("BA_ATTN_2CTA");
-    two_cta = env && atoi(env) ? 1 : 0;
+// B = 128 kernel choice, BA_ATTN_K5 = "pp" (ping-pong pair, attn_sm100_pp.cu),
+// "2cta" (cluster pair, attn_sm100_2cta.cu) or "1cta" (attn_sm100.cu).  The pair
+// kernels walk the union of two adjacent query blocks' lists.
+enum K5Kind { K5_1CTA = 0, K5_2CTA = 1, K5_PP = 2 };
+static const int kDefaultK5 = K5_1CTA;
+
+static int k5_kind() {
+  static int kind = -1;
+  if (kind < 0) {
+    kind = kDefaultK5;
+    const char *env = getenv("BA_ATTN_K5");
+    if (env && !strcmp(env, "pp")) kind = K5_PP;
+    else if (env && !strcmp(env, "2cta")) kind = K5_2CTA;
+    else if (env && !strcmp(env, "1cta")) kind = K5_1CTA;
+    else if (getenv("BA_ATTN_2CTA") && atoi(getenv("BA_ATTN_2CTA"))) kind = K5_2CTA;
   }
-  return two_cta && attn_2cta_supported(a);
+  return kind;
 }
 
+bool use_pp(const AttnArgs &a) { return k5_kind() == K5_PP && attn_pp_supported(a); }
+bool use_2cta(const AttnArgs &a) { return k5_kind() == K5_2CTA && attn_2cta_supported(a); }
+
 const char *attn_kernel_name(const AttnArgs &a) {
+  if (use_pp(a)) return "attn_sm100_tcgen05_pp";
   if (use_2cta(a)) return "attn_sm100_tcgen05_2cta";
   return attn_sm100_supported(a) ? "attn_sm100_tcgen05" : "attn_simt";
 }
 
 ba_status run_attn(const AttnArgs &a, cudaStream_t st) {
   cudaError_t e;
-  if (use_2cta(a)) e = launch_attn_2cta(a, st);
+  if (use_pp(a)) e = launch_attn_pp(a, st);
+  else if (use_2cta(a)) e = launch_attn_2cta(a, st);
   else if (attn_sm100_supported(a)) e = launch_attn_sm100(a, st);
   else e = launch_attn_simt(a, st);
   g_launches = 1;

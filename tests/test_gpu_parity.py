@@ -179,15 +179,13 @@ def test_injected_oracle_mask(ba):
     assert ref_sel  # oracle selection computed on the same inputs
 
 
-@pytest.mark.parametrize("B,two_cta", [(128, False), (128, True), (64, False)])
-def test_injected_dissimilar_lists(ba, B, two_cta):
+@pytest.mark.parametrize("B,k5", [(128, "1cta"), (128, "2cta"), (128, "pp"), (64, "1cta")])
+def test_injected_dissimilar_lists(ba, B, k5):
     """Random (dissimilar) index lists for every query block: exercises the
     pair kernels' union walk where a block skips tiles (P = 0 rows), including
     a skipped LAST tile (the epilogue must still wait for every PV)."""
     import subprocess, sys, os
-    env = dict(os.environ)
-    if two_cta:
-        env["BA_ATTN_2CTA"] = "1"
+    env = dict(os.environ, BA_ATTN_K5=k5)
     code = f"""
 import sys; sys.path.insert(0, {os.path.join(os.path.dirname(__file__))!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
 import numpy as np, torch
@@ -238,11 +236,13 @@ def test_errors_are_loud(ba):
         ba.ba_attention(q, k, v)
 
 
-def test_two_cta_kernel_parity(ba):
-    """The opt-in 2-CTA cluster kernel (BA_ATTN_2CTA=1) on real selections,
+@pytest.mark.parametrize("k5,name", [("2cta", "attn_sm100_tcgen05_2cta"), ("pp", "attn_sm100_tcgen05_pp"),
+                                     ("1cta", "attn_sm100_tcgen05")])
+def test_b128_kernel_parity(ba, k5, name):
+    """Each B = 128 kernel (BA_ATTN_K5 = 2cta | pp | 1cta) on real selections,
     ragged lengths, GQA and an odd number of query blocks."""
     import os, subprocess, sys
-    env = dict(os.environ, BA_ATTN_2CTA="1")
+    env = dict(os.environ, BA_ATTN_K5=k5)
     code = f"""
 import sys; sys.path.insert(0, {os.path.dirname(__file__)!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
 import torch
@@ -262,4 +262,4 @@ for cfg, L, hq, hkv, dens in (("A", 4096 + 77, 2, 2, 0.5), ("C", 3 * 128 * 5, 4,
 print("OK", ba.attention_kernel_name(q, k, v, 128))
 """
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=240)
-    assert r.returncode == 0 and "OK attn_sm100_tcgen05_2cta" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.returncode == 0 and f"OK {name}\n" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

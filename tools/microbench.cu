@@ -55,7 +55,94 @@ __global__ void ffma2_kernel(float *out, int iters, long long *cyc) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
-int main() {
+// cvt.rn.bf16x2.f32 (F2FP.BF16.F32.PACK_AB) throughput
+__global__ void f2fp_kernel(float *out, int iters, long long *cyc) {
+  float x[8];
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3f + i * 1e-4f;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t r;
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x[i]), "f"(x[(i + 1) & 7]));
+      x[i] = __uint_as_float(r);
+    }
+  }
+  long long t1 = clock64();
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+// the softmax inner step per pair: ffma2, 2 x ex2, fadd2, cvt.bf16x2 (mode 0) or
+// the same with the pack done by integer ops (mode 1: add 0x7fff + lsb, prmt)
+template <int kMode>
+__global__ void pair_kernel(float *out, int iters, long long *cyc) {
+  uint64_t x[8], acc4[4] = {0, 0, 0, 0}, c2, m2;
+  uint32_t pk = 0;
+  for (int i = 0; i < 8; ++i) asm("mov.b64 %0, {%1, %1};" : "=l"(x[i]) : "f"(-(threadIdx.x * 1e-3f + i)));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(c2) : "f"(0.5f));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(m2) : "f"(-0.25f));
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint64_t y;
+      asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(y) : "l"(x[i]), "l"(c2), "l"(m2));
+      x[i] = y;
+      float lo, hi;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(y));
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(lo));
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(hi));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(lo), "f"(hi));
+      asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(acc4[i & 3]) : "l"(y));
+      uint32_t r;
+      if (kMode == 0) {
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+      } else {
+        const uint32_t a = __float_as_uint(lo) + 0x8000u, b = __float_as_uint(hi) + 0x8000u;
+        asm volatile("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(a), "r"(b));
+      }
+      pk ^= r;
+    }
+  }
+  long long t1 = clock64();
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc4[0] ^ acc4[1] ^ acc4[2] ^ acc4[3]));
+  out[blockIdx.x * blockDim.x + threadIdx.x] = lo + hi + (float)pk;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <typename K>
+double run(K kern, int warps, int iters, float *out, long long *cyc) {
+  long long h[148];
+  kern<<<148, warps * 32>>>(out, iters, cyc);
+  cudaDeviceSynchronize();
+  cudaMemcpy(h, cyc, 148 * 8, cudaMemcpyDeviceToHost);
+  double c = 0;
+  for (int i = 0; i < 148; ++i) c += h[i];
+  return c / 148;
+}
+
+int main(int argc, char **argv) {
+  if (argc > 1) {  // softmax-step modes only
+    float *out; long long *cyc;
+    cudaMalloc(&out, 148 * 1024 * 4); cudaMalloc(&cyc, 148 * 8);
+    for (int warps : {4, 8}) {
+      const int iters = 2048;
+      double c = run(f2fp_kernel, warps, iters, out, cyc);
+      printf("cvt.bf16x2 warps/SM=%2d: %.2f cvt/clk/SM\n", warps, warps * 32.0 * iters * 8 / c);
+      c = run(pair_kernel<0>, warps, iters, out, cyc);
+      printf("pair(cvt)  warps/SM=%2d: %.2f exp/clk/SM  (%.1f cyc per 64-pair row-tile per warp)\n", warps,
+             warps * 32.0 * iters * 16 / c, c / iters / 8 * 64 / (warps / 4.0));
+      c = run(pair_kernel<1>, warps, iters, out, cyc);
+      printf("pair(prmt) warps/SM=%2d: %.2f exp/clk/SM  (%.1f cyc per 64-pair row-tile per warp)\n", warps,
+             warps * 32.0 * iters * 16 / c, c / iters / 8 * 64 / (warps / 4.0));
+    }
+    printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+  }
   float *out; long long *cyc;
   cudaMalloc(&out, 148 * 1024 * 4); cudaMalloc(&cyc, 148 * 8);
   long long h[148];
