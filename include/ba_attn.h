@@ -83,7 +83,13 @@ typedef enum { BA_SORT_NONE = 0, BA_SORT_Q = 1, BA_SORT_K = 2, BA_SORT_QK = 3 } 
 typedef enum { BA_COMP_NONE = 0, BA_COMP_DIAG = 1 } ba_comp_mode;
 
 /* Budget rule ("under different computational budgets"; Alg. 1 step 10
- * P:560 top-kappa).  TOPP (cumulative mass >= top_p) is reserved. */
+ * P:560 top-kappa).
+ *   BA_SELECT_TOPK  every query block keeps kappa = round(density*N_k) blocks.
+ *   BA_SELECT_TOPP  cumulative mass (reading A23): order a row by
+ *                   (-m', g_k) and keep the shortest prefix whose mass reaches
+ *                   top_p, at most kappa(density) blocks (density = 1: no cap);
+ *                   kv_count[row] = that length, kv_index rows keep the
+ *                   capacity kappa(density) as their stride. */
 typedef enum { BA_SELECT_TOPK = 0, BA_SELECT_TOPP = 1 } ba_select_mode;
 
 typedef struct {
@@ -108,7 +114,7 @@ typedef struct {
   float beta;            /* compensation weight; default 1 */
   int32_t select;        /* ba_select_mode; BA_SELECT_TOPK */
   float density;         /* rho in (0, 1]; kappa = max(1, min(N_k, floor(rho*N_k + 1/2))) (reading A2) */
-  float top_p;           /* BA_SELECT_TOPP only (reserved) */
+  float top_p;           /* BA_SELECT_TOPP only: in (0, 1] (else BA_ERR_INVALID_ARGUMENT) */
   float softmax_scale;   /* 0 => 1/sqrt(head_dim) (Eq. sdpa) */
 } ba_params;
 
@@ -123,11 +129,11 @@ typedef struct {
   void *k_sorted;        /* [b, H_kv, L_k, d] contiguous: K'_j = K_{pi_k(j)} */
   void *v_sorted;        /* [b, H_kv, L_k, d] contiguous: V'_j = V_{pi_k(j)} */
   int32_t *kv_index;     /* [b, H_q, N_q, kappa] selected key blocks g_k, strictly ascending */
-  int32_t *kv_count;     /* [b, H_q, N_q] number of valid entries per row (== kappa for TOPK) */
+  int32_t *kv_count;     /* [b, H_q, N_q] number of valid entries per row (== kappa for TOPK, <= kappa for TOPP) */
   uint8_t *mask;         /* [b, H_q, N_q, N_k] M in {0,1} */
   double *block_prob;    /* [b, H_q, N_q, N_k] m' = softmax_row(l') */
   double *logits;        /* [b, H_q, N_q, N_k] l' = l + beta*Delta */
-  double *threshold;     /* [b, H_q, N_q] tau = m' of the kappa-th selected block */
+  double *threshold;     /* [b, H_q, N_q] tau = m' of the last (kv_count-th largest) selected block */
   double *q_mean;        /* [b, H_q, N_q, d] Qbar over the sorted blocks */
   double *q_var;         /* [b, H_q, N_q, d] population variance per dimension */
   double *k_mean;        /* [b, H_kv, N_k, d] */

@@ -20,7 +20,7 @@ reordering beyond what the cited definition states.
 Pin status (see tests/test_oracle_pins.py):
   norm_key, norm_rank, apply/unapply_permutation, make_grid, block_stats,
   block_logits, compensation_diag, compensation_exact, softmax_rows,
-  kappa_from_density, topk_mask, select_head, block_sparse_attention_head,
+  kappa_from_density, topk_mask, topp_mask, select_head, block_sparse_attention_head,
   dense_attention, oracle_block_mass, deviation_bound, lemma_check,
   ba_attention — all pinned (closed forms, worked examples, brute force,
   invariants).  Nothing here is "parity unpinned".
@@ -201,6 +201,38 @@ def topk_mask(m, kappa: int):
     return mask, tau, idx
 
 
+def topp_mask(m, top_p: float, kappa_cap: int):
+    """Cumulative-mass budget (NEXT-1; the paper builds M from m' "under
+    different computational budgets").  Reading A23: per row, order the
+    key blocks by (-m', g_k) as in top-kappa (reading A3) and keep the shortest
+    prefix whose cumulative mass reaches top_p:
+        kappa_row = min{k >= 1 : sum_{r<k} m'_(r) >= top_p}   (N_k if none),
+    then cap it at kappa_cap (the density budget; density 1 = no cap).  The
+    cumulative sum runs sequentially in that order, in fp64.  Returns (mask,
+    tau = m' of the last kept entry, kv_index as a list of ascending arrays,
+    kappa_row[Nq])."""
+    m = _f64(m)
+    nq, nk = m.shape
+    assert 0.0 < top_p <= 1.0 and 1 <= kappa_cap <= nk
+    mask = np.zeros((nq, nk), dtype=np.uint8)
+    tau = np.zeros(nq, dtype=np.float64)
+    kap = np.zeros(nq, dtype=np.int64)
+    idx = []
+    cols = np.arange(nk)
+    for r in range(nq):
+        order = np.lexsort((cols, -m[r]))
+        cum = np.cumsum(m[r, order])
+        hit = np.nonzero(cum >= top_p)[0]
+        k = int(hit[0]) + 1 if hit.size else nk
+        k = min(k, kappa_cap)
+        chosen = order[:k]
+        mask[r, chosen] = 1
+        tau[r] = m[r, order[k - 1]]
+        kap[r] = k
+        idx.append(np.sort(chosen))
+    return mask, tau, idx, kap
+
+
 @dataclass
 class Selection:
     perm_q: np.ndarray
@@ -223,10 +255,12 @@ class Selection:
 def select_head(Q, K, B: int, density: float, beta: float = 1.0,
                 sort: int = SORT_QK, comp: int = COMP_DIAG,
                 window: Optional[int] = None,
-                perm_q=None, perm_k=None) -> Selection:
+                perm_q=None, perm_k=None, top_p: Optional[float] = None) -> Selection:
     """Algorithm 1 steps 1-10 for one (batch, q-head) with its
     key head.  ``perm_q``/``perm_k`` may be supplied (e.g. shared K-side
-    permutation under GQA) — otherwise computed here."""
+    permutation under GQA) — otherwise computed here.  ``top_p``: the
+    cumulative-mass budget (reading A23) instead of top-kappa, capped at the
+    density's kappa; ``kv_index`` is then a list of per-row arrays."""
     Q, K = _f64(Q), _f64(K)
     d = Q.shape[1]
     if perm_q is None:  # step 1
@@ -246,9 +280,14 @@ def select_head(Q, K, B: int, density: float, beta: float = 1.0,
     lp = l + float(beta) * delta                    # step 7
     m = softmax_rows(lp)                            # step 9
     kappa = kappa_from_density(density, l.shape[1])
-    mask, tau, idx = topk_mask(m, kappa)            # step 10
+    extra = {}
+    if top_p is None:
+        mask, tau, idx = topk_mask(m, kappa)        # step 10
+    else:
+        mask, tau, idx, extra["kappa_row"] = topp_mask(m, top_p, kappa)
+        extra["top_p"] = float(top_p)
     return Selection(np.asarray(perm_q), np.asarray(perm_k), q_mean, q_var, k_mean, k_var,
-                     l, delta, lp, m, mask, tau, idx, kappa)
+                     l, delta, lp, m, mask, tau, idx, kappa, extra)
 
 
 # --------------------------------------------------------------------------
@@ -359,6 +398,7 @@ class Params:
     comp: int = COMP_DIAG
     window: Optional[int] = None
     scale: Optional[float] = None
+    top_p: Optional[float] = None   # cumulative-mass budget (reading A23); None = top-kappa
 
 
 def ba_attention(Q, K, V, p: Params, q_blocks: Optional[dict] = None,
@@ -386,13 +426,13 @@ def ba_attention(Q, K, V, p: Params, q_blocks: Optional[dict] = None,
             if selections is not None:
                 perm_q, perm_k, kv_index = selections[(bi, h)]
                 perm_q, perm_k = np.asarray(perm_q), np.asarray(perm_k)
-                kv_index = np.asarray(kv_index)
+                kv_index = [np.asarray(r) for r in kv_index]
             else:
                 if hk not in kperm_cache:
                     kperm_cache[hk] = (norm_rank(K[bi, hk], p.window) if p.sort in (SORT_K, SORT_QK)
                                        else np.arange(K.shape[2]))
                 sel = select_head(Q[bi, h], K[bi, hk], p.block_size, p.density, p.beta,
-                                  p.sort, p.comp, p.window, perm_k=kperm_cache[hk])
+                                  p.sort, p.comp, p.window, perm_k=kperm_cache[hk], top_p=p.top_p)
                 sels[(bi, h)] = sel
                 perm_q, perm_k, kv_index = sel.perm_q, sel.perm_k, sel.kv_index
             Qs = apply_permutation(Q[bi, h], perm_q)
@@ -410,7 +450,7 @@ def sparse_flops(kv_index, Lq: int, Lk: int, B: int, d: int, dv: Optional[int] =
     dv = d if dv is None else dv
     gq, gk = make_grid(Lq, B), make_grid(Lk, B)
     tot = 0
-    for g, row in enumerate(np.asarray(kv_index)):
+    for g, row in enumerate(kv_index):
         nq = gq[g][1] - gq[g][0]
         for j in row:
             nk = gk[int(j)][1] - gk[int(j)][0]

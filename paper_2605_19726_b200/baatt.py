@@ -235,9 +235,13 @@ class Context:
     (the bench's timed loop calls the library without re-allocating)."""
 
     def __init__(self, q, k, v, block_size=128, density=0.5, beta=1.0, sort="qk", comp="diag",
-                 sort_window=0, softmax_scale=0.0, diagnostics=False, out=None):
+                 sort_window=0, softmax_scale=0.0, diagnostics=False, out=None, top_p=None):
+        """top_p: None = top-kappa (Alg. 1 step 10); a float in (0, 1] = the
+        cumulative-mass budget (reading A23), capped at kappa(density)."""
         self.prob = make_problem(q, k, v, out, block_size)
-        self.params = make_params(density, beta, sort, comp, sort_window, softmax_scale)
+        select = SELECT_TOPK if top_p is None else SELECT_TOPP
+        self.params = make_params(density, beta, sort, comp, sort_window, softmax_scale, select,
+                                  0.0 if top_p is None else top_p)
         lib = load()
         self.ws_select = _workspace(lib.ba_select_workspace_size(ctypes.byref(self.prob), ctypes.byref(self.params)), q.device)
         self.sel = alloc_selection(q, k, self.prob, self.params, diagnostics)
@@ -257,8 +261,8 @@ class Context:
 
 
 def ba_select(q, k, v, block_size=128, density=0.5, beta=1.0, sort="qk", comp="diag", sort_window=0,
-              diagnostics=False, stream=None) -> Selection:
-    ctx = Context(q, k, v, block_size, density, beta, sort, comp, sort_window, 0.0, diagnostics)
+              diagnostics=False, stream=None, top_p=None) -> Selection:
+    ctx = Context(q, k, v, block_size, density, beta, sort, comp, sort_window, 0.0, diagnostics, top_p=top_p)
     return ctx.select(q, k, v, stream)
 
 
@@ -276,11 +280,12 @@ def ba_sparse_attn(q, k, v, sel: Selection, block_size=128, density=0.5, softmax
 
 
 def ba_attention(q, k, v, block_size=128, density=0.5, beta=1.0, sort="qk", comp="diag", sort_window=0,
-                 softmax_scale=0.0, out=None, lse=None, workspace=None, stream=None):
+                 softmax_scale=0.0, out=None, lse=None, workspace=None, stream=None, top_p=None):
     if out is None:
         out = torch.empty_like(q)
     prob = make_problem(q, k, v, out, block_size)
-    params = make_params(density, beta, sort, comp, sort_window, softmax_scale)
+    params = make_params(density, beta, sort, comp, sort_window, softmax_scale,
+                         SELECT_TOPK if top_p is None else SELECT_TOPP, 0.0 if top_p is None else top_p)
     lib = load()
     need = lib.ba_attention_workspace_size(ctypes.byref(prob), ctypes.byref(params))
     if workspace is None or workspace.numel() < need:

@@ -66,10 +66,9 @@ ba_status check_problem(const ba_problem *p, const ba_params *pa, Dims *o) {
   if (p->dtype != BA_DTYPE_BF16 && p->dtype != BA_DTYPE_FP32) return fail(BA_ERR_INVALID_ARGUMENT, "dtype = %d", p->dtype);
   if (pa->sort < BA_SORT_NONE || pa->sort > BA_SORT_QK) return fail(BA_ERR_INVALID_ARGUMENT, "sort = %d", pa->sort);
   if (pa->comp != BA_COMP_NONE && pa->comp != BA_COMP_DIAG) return fail(BA_ERR_INVALID_ARGUMENT, "comp = %d", pa->comp);
-  if (pa->select != BA_SELECT_TOPK) {
-    if (pa->select == BA_SELECT_TOPP) return fail(BA_ERR_UNSUPPORTED, "select = BA_SELECT_TOPP is reserved");
-    return fail(BA_ERR_INVALID_ARGUMENT, "select = %d", pa->select);
-  }
+  if (pa->select != BA_SELECT_TOPK && pa->select != BA_SELECT_TOPP) return fail(BA_ERR_INVALID_ARGUMENT, "select = %d", pa->select);
+  if (pa->select == BA_SELECT_TOPP && !(pa->top_p > 0.f && pa->top_p <= 1.f))
+    return fail(BA_ERR_INVALID_ARGUMENT, "top_p = %g not in (0, 1]", (double)pa->top_p);
   if (!(pa->density > 0.f && pa->density <= 1.f)) return fail(BA_ERR_INVALID_ARGUMENT, "density = %g not in (0, 1]", (double)pa->density);
   if (!(pa->softmax_scale >= 0.f) || !isfinite(pa->softmax_scale)) return fail(BA_ERR_INVALID_ARGUMENT, "softmax_scale = %g", (double)pa->softmax_scale);
   if (!isfinite(pa->beta)) return fail(BA_ERR_INVALID_ARGUMENT, "beta is not finite");
@@ -247,7 +246,8 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   double *logits = sel->logits ? sel->logits : at<double>(ws, plan.logits);
   BA_TRY(cuda_check(launch_scores((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, q_var, k_mean, k_var,
                                   pa->comp == BA_COMP_DIAG ? 1 : 0, (double)pa->beta, logits, st), "scores"));
-  BA_TRY(cuda_check(launch_topk(D.b * D.hq * D.nq, D.nk, D.kappa, logits, sel->kv_index, sel->kv_count,
+  const double top_p = pa->select == BA_SELECT_TOPP ? (double)pa->top_p : 0.0;
+  BA_TRY(cuda_check(launch_topk(D.b * D.hq * D.nq, D.nk, D.kappa, top_p, logits, sel->kv_index, sel->kv_count,
                                 sel->mask, sel->block_prob, sel->threshold, st), "topk"));
   launches += 2;
   g_launches = launches;

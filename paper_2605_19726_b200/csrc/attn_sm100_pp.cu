@@ -74,6 +74,7 @@ struct __align__(8) Bars {
   uint64_t q_full;
   uint64_t full[NSLOT], empty[NSLOT];
   uint64_t s_full[2], p_full[2];  // per query block (A, B)
+  uint64_t tok[2][4];             // MUFU token per SMSP: softmax A(u) -> B(u) -> A(u+1) ...
   uint64_t o_final;
   uint32_t tmem_base;
   uint32_t n_union;
@@ -99,7 +100,7 @@ struct UnionWalk {
 // (0,0) prints clock64 stamps of its first kTraceTiles union tiles, BA_ATTN_DEBUG=2).
 // kEmu: of every 8 exp2 pairs, kEmu are evaluated by a polynomial on the FMA
 // pipe instead of MUFU (BA_EXP_EMU).
-template <int kMode, int kEmu>
+template <int kMode, int kEmu, bool kStagger = true>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v) {
@@ -157,6 +158,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       mbar_init(&bars.q_full, 1);
       for (int s = 0; s < NSLOT; ++s) { mbar_init(&bars.full[s], 1); mbar_init(&bars.empty[s], 1); }
       for (int s = 0; s < 2; ++s) { mbar_init(&bars.s_full[s], 1); mbar_init(&bars.p_full[s], 4); }
+      for (int s = 0; s < 8; ++s) mbar_init(&bars.tok[s >> 2][s & 3], 1);
       mbar_init(&bars.o_final, 1);
       fence_barrier_init();
       tma_prefetch(&tm_q);
@@ -271,6 +273,18 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     uint32_t sr[128];
     UnionWalk walk;
     walk.init(mask_a, mask_b);
+    // MUFU stagger: the A and B softmax warps sharing an SMSP (same qd) take turns
+    // on the exp section, A(u), B(u), A(u+1), ... so that one exponentiates while
+    // the tensor pipe runs the other's PV + next S (the tile trace showed both in
+    // phase, splitting MUFU, with the tensor pipe idle meanwhile).
+    auto take_token = [&](int u) {
+      if (x == 1) mbar_wait(&bars.tok[1][qd], (uint32_t)u & 1u);
+      else if (u > 0) mbar_wait(&bars.tok[0][qd], (uint32_t)(u - 1) & 1u);
+    };
+    auto give_token = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.tok[x ^ 1][qd]);
+    };
     for (int u = 0; u < cnt; ++u) {
       const int gk = walk.next();
       const bool mine = (my_mask[gk >> 5] >> (gk & 31)) & 1u;  // warpgroup-uniform
@@ -319,6 +333,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
             l *= corr;
           }
         }
+        if (kStagger) take_token(u);
         const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
@@ -341,8 +356,10 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         float a0, a1;
         unf2(t2, a0, a1);
         l += a0 + a1;
+        if (kStagger) give_token();
         if (trx) TR(6 + 4 * x, u);
       } else {
+        if (kStagger) { take_token(u); give_token(); }
 #pragma unroll
         for (int i = 0; i < 64; ++i) sr[i] = 0u;  // block not selected by these rows: P = 0
       }
@@ -401,16 +418,17 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
 
 namespace sm100 {
 namespace pp {
-template <int kMode, int kEmu>
+template <int kMode, int kEmu, bool kStagger = true>
 cudaError_t launch_mode(const AttnArgs &a, const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, dim3 grid,
                         cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel<kMode, kEmu>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel<kMode, kEmu, kStagger>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  attn_pp_kernel<kMode, kEmu><<<grid, kThreads, SMEM_BYTES, st>>>(a, mq, mk, mv);
+  attn_pp_kernel<kMode, kEmu, kStagger><<<grid, kThreads, SMEM_BYTES, st>>>(a, mq, mk, mv);
   return cudaGetLastError();
 }
 }  // namespace pp
@@ -428,8 +446,10 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
   if (!make_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs, 128) || !make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) ||
       !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128))
     return cudaErrorInvalidValue;
-  static int dbg = -1, emu = -1;
+  static int dbg = -1, emu = -1, stagger = 1;
   if (dbg < 0) {
+    const char *sg = getenv("BA_PP_STAGGER");
+    stagger = sg ? atoi(sg) : 1;
     const char *d = getenv("BA_ATTN_DEBUG");
     dbg = d ? atoi(d) : 0;
     if (dbg < 0 || dbg > 2) dbg = 0;
@@ -439,7 +459,9 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
   }
   dim3 grid((unsigned)((a.nq + 1) / 2), (unsigned)(a.batch * a.hq));
   if (dbg == 1) return launch_mode<1, 0>(a, mq, mk, mv, grid, st);
-  if (dbg == 2) return launch_mode<2, kDefaultEmu>(a, mq, mk, mv, grid, st);
+  if (dbg == 2) return stagger ? launch_mode<2, kDefaultEmu>(a, mq, mk, mv, grid, st)
+                               : launch_mode<2, kDefaultEmu, false>(a, mq, mk, mv, grid, st);
+  if (!stagger) return launch_mode<0, kDefaultEmu, false>(a, mq, mk, mv, grid, st);
   switch (emu) {
     case 0: return launch_mode<0, 0>(a, mq, mk, mv, grid, st);
     case 1: return launch_mode<0, 1>(a, mq, mk, mv, grid, st);

@@ -24,6 +24,8 @@
 //                    exact kappa-th largest l' by a 64-step radix select on
 //                    order-preserving bits, ties -> lower g_k, ascending index
 //                    list + mask.  One warp per row, row in smem.
+//                    TOPP (reading A23): kappa_row from the cumulative mass
+//                    of the (-m', g_k)-ordered row, capped at kappa.
 #include <math.h>
 
 #include "common.cuh"
@@ -541,7 +543,93 @@ cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t
 // =====================================================================================
 // K4b: per-row top-kappa.  One warp per row; the row's l' values sit in smem.
 // =====================================================================================
-__global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, const double *__restrict__ logits,
+// Order-preserving bits of a non-negative double back to its value.
+BA_DEVICE double unordered_pos(uint64_t u) { return __longlong_as_double((long long)(u ^ 0x8000000000000000ull)); }
+
+// Warp sum in a fixed order (lane-strided sequential partials, then an xor
+// tree): deterministic, so reruns give bit-identical kappa_row.
+BA_DEVICE double warp_sum_det(double v) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// Cumulative-mass budget (reading A23, NEXT-1): kappa_row = the length of the
+// shortest (-m', g_k)-ordered prefix whose mass reaches p.  u[] holds the
+// order-preserving bits of m' (>= 0).  A 16-pass MSD radix select with 4-bit
+// digits finds the value T of the crossing entry: per pass every lane keeps
+// 16 fp64 bucket masses and counts of the candidates sharing the prefix in
+// registers, reduced deterministically across the warp; the digit where the
+// running mass (from the top) reaches p is kept.  Then entries > T are counted
+// and summed once more, and the entries equal to T are added (ascending g_k)
+// until the mass reaches p.
+BA_DEVICE unsigned topp_count(const uint64_t *u, int64_t nk, double p, double total, int lane) {
+  if (total < p) return (unsigned)nk;  // the whole row does not reach p: keep everything
+  uint64_t T = 0, pmask = 0;
+  double above = 0.0;  // mass of the entries above the current prefix range
+  for (int pass = 0; pass < 16; ++pass) {
+    const int shift = 60 - 4 * pass;
+    double acc[16];
+    unsigned cnt[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) { acc[b] = 0.0; cnt[b] = 0u; }
+    for (int64_t j = lane; j < nk; j += 32) {
+      const uint64_t v = u[j];
+      if ((v & pmask) == T) {
+        const unsigned dg = (unsigned)(v >> shift) & 15u;
+        const double val = unordered_pos(v);
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+          const bool hit = dg == (unsigned)b;
+          acc[b] += hit ? val : 0.0;
+          cnt[b] += hit ? 1u : 0u;
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+      acc[b] = warp_sum_det(acc[b]);
+      cnt[b] = __reduce_add_sync(0xffffffffu, cnt[b]);
+    }
+    // the crossing digit; if fp64 re-association leaves no crossing, the lowest non-empty digit
+    int dsel = -1, lowest = -1;
+    double run = above;
+#pragma unroll
+    for (int b = 15; b >= 0; --b) {
+      if (!cnt[b]) continue;
+      lowest = b;
+      if (dsel < 0) {
+        if (run + acc[b] >= p) dsel = b;
+        else run += acc[b];
+      }
+    }
+    if (dsel < 0) dsel = lowest;
+#pragma unroll
+    for (int b = 15; b >= 0; --b)
+      if (b > dsel) above += acc[b];
+    T |= (uint64_t)dsel << shift;
+    pmask |= 0xFull << shift;
+  }
+  // exact pass: entries strictly above T, then T's ties in ascending g_k
+  double s_gt = 0.0;
+  unsigned c_gt = 0, c_eq = 0;
+  for (int64_t j = lane; j < nk; j += 32) {
+    const uint64_t v = u[j];
+    if (v > T) { s_gt += unordered_pos(v); ++c_gt; }
+    c_eq += v == T;
+  }
+  s_gt = warp_sum_det(s_gt);
+  c_gt = __reduce_add_sync(0xffffffffu, c_gt);
+  c_eq = __reduce_add_sync(0xffffffffu, c_eq);
+  const double tv = unordered_pos(T);
+  unsigned need = 0;
+  double cum = s_gt;
+  while (need < c_eq && cum < p) { cum += tv; ++need; }
+  if (need == 0) need = 1;  // s_gt >= p only through re-association: a near-tie inside the band
+  return c_gt + need;
+}
+
+__global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *__restrict__ logits,
                             int32_t *__restrict__ kv_index, int32_t *__restrict__ kv_count,
                             uint8_t *__restrict__ mask, double *__restrict__ prob,
                             double *__restrict__ tau) {
@@ -561,14 +649,24 @@ __global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, const doubl
 #pragma unroll
   for (int off = 16; off; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
   __syncwarp();
-  double denom = 0.0;
-  const bool need_prob = (prob != nullptr) || (tau != nullptr);
+  double denom = 0.0, total = 0.0;
+  const bool topp = top_p > 0.0;
+  const bool need_prob = (prob != nullptr) || (tau != nullptr) || topp;
   if (need_prob) {
     for (int64_t j = lane; j < nk; j += 32) denom += exp(x[j] - mx);
 #pragma unroll
     for (int off = 16; off; off >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, off);
-    if (prob)
+    if (topp) {  // rank by m' itself (reading A23 orders by (-m', g_k))
+      for (int64_t j = lane; j < nk; j += 32) {
+        const double mp = exp(x[j] - mx) / denom;
+        x[j] = mp;
+        total += mp;
+        if (prob) prob[row * nk + j] = mp;
+      }
+      total = warp_sum_det(total);
+    } else if (prob) {
       for (int64_t j = lane; j < nk; j += 32) prob[row * nk + j] = exp(x[j] - mx) / denom;
+    }
   }
   // kappa-th largest ordered key by an 8-pass MSD radix select (8-bit digits):
   // per pass, histogram the digit of the candidates sharing the current prefix
@@ -579,7 +677,12 @@ __global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, const doubl
   const uint64_t *u = reinterpret_cast<const uint64_t *>(x);
   unsigned *hist = hist_base + warp * 256;
   uint64_t T = 0, pmask = 0;
-  unsigned k_rem = (unsigned)kappa;
+  unsigned k_rem = (unsigned)kappa;  // TOPK: kappa; TOPP: min(kappa_row, kappa) (kappa = the density cap)
+  if (topp) {
+    const unsigned kp = topp_count(u, nk, top_p, total, lane);
+    if (kp < k_rem) k_rem = kp;
+  }
+  const unsigned k_row = k_rem;
   for (int pass = 0; pass < 8; ++pass) {
     const int shift = 56 - 8 * pass;
 #pragma unroll
@@ -637,16 +740,18 @@ __global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, const doubl
     eq_seen += __popc(eqm);
     sel_seen += __popc(selm);
   }
-  if (lane == 0) kv_count[row] = (int32_t)kappa;
+  if (lane == 0) kv_count[row] = (int32_t)k_row;
   if (tau && lane == 0) {
-    // invert the order-preserving map: T holds the kappa-th largest l' exactly
+    // invert the order-preserving map: T holds the kappa-th largest l' (TOPP: m') exactly
     const uint64_t tb = (T >> 63) ? (T ^ 0x8000000000000000ull) : ~T;
-    tau[row] = exp(__longlong_as_double((long long)tb) - mx) / denom;
+    const double tval = __longlong_as_double((long long)tb);
+    tau[row] = topp ? tval : exp(tval - mx) / denom;
   }
 }
 
-cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, const double *logits, int32_t *kv_index,
-                        int32_t *kv_count, uint8_t *mask, double *prob, double *tau, cudaStream_t st) {
+cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *logits,
+                        int32_t *kv_index, int32_t *kv_count, uint8_t *mask, double *prob, double *tau,
+                        cudaStream_t st) {
   int warps = 8;
   while (warps > 1 && (size_t)warps * (nk * sizeof(double) + 1024) > 160 * 1024) warps >>= 1;
   const size_t smem = (size_t)warps * (nk * sizeof(double) + 256 * sizeof(unsigned));
@@ -655,7 +760,7 @@ cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, const double *l
     if (e != cudaSuccess) return e;
   }
   const unsigned grid = (unsigned)((rows + warps - 1) / warps);
-  topk_kernel<<<grid, warps * 32, smem, st>>>(rows, nk, kappa, logits, kv_index, kv_count, mask, prob, tau);
+  topk_kernel<<<grid, warps * 32, smem, st>>>(rows, nk, kappa, top_p, logits, kv_index, kv_count, mask, prob, tau);
   return cudaGetLastError();
 }
 

@@ -22,7 +22,7 @@ SORT_CODE = {"none": O.SORT_NONE, "q": O.SORT_Q, "k": O.SORT_K, "qk": O.SORT_QK}
 COMP_CODE = {"none": O.COMP_NONE, "diag": O.COMP_DIAG}
 
 
-def oracle_select_all(q, k, B, density, beta, sort, comp, window=None, heads=None):
+def oracle_select_all(q, k, B, density, beta, sort, comp, window=None, heads=None, top_p=None):
     """Oracle selection for every (b, hq) (or the listed heads) on the exact
     tensors the GPU consumed."""
     b, hq = q.shape[0], q.shape[1]
@@ -38,7 +38,7 @@ def oracle_select_all(q, k, B, density, beta, sort, comp, window=None, heads=Non
                 kcache[(bi, hk)] = (O.norm_rank(kn[bi, hk], window) if SORT_CODE[sort] in (O.SORT_K, O.SORT_QK)
                                     else np.arange(kn.shape[2]))
             out[(bi, h)] = O.select_head(qn[bi, h], kn[bi, hk], B, density, beta, SORT_CODE[sort],
-                                         COMP_CODE[comp], window, perm_k=kcache[(bi, hk)])
+                                         COMP_CODE[comp], window, perm_k=kcache[(bi, hk)], top_p=top_p)
     return out
 
 
@@ -57,15 +57,33 @@ def check_selection(sel, ref: dict, band: float = MASK_BAND, check_stats: bool =
     for (bi, h), r in ref.items():
         hk = h // grp
         rep["perm_mismatch"] += int((perm_q[bi, h] != r.perm_q).sum()) + int((perm_k[bi, hk] != r.perm_k).sum())
-        assert (kv_count[bi, h] == r.kappa).all(), "kv_count != kappa"
-        idx = kv_index[bi, h]
-        assert (np.diff(idx, axis=1) > 0).all(), "kv_index rows must be strictly ascending"
         gmask = np.zeros_like(r.mask)
-        np.put_along_axis(gmask, idx.astype(np.int64), 1, axis=1)
+        if "kappa_row" not in r.extra:  # top-kappa: every row keeps exactly kappa
+            assert (kv_count[bi, h] == r.kappa).all(), "kv_count != kappa"
+            idx = kv_index[bi, h]
+            assert (np.diff(idx, axis=1) > 0).all(), "kv_index rows must be strictly ascending"
+            np.put_along_axis(gmask, idx.astype(np.int64), 1, axis=1)
+            near = np.abs(r.m - r.tau[:, None]) <= band
+        else:  # top-p (reading A23): kappa_row may differ only where the cumulative mass ties p
+            kr = r.extra["kappa_row"]
+            near = np.abs(r.m - r.tau[:, None]) <= band
+            for g in range(kr.shape[0]):
+                c = int(kv_count[bi, h, g])
+                row = kv_index[bi, h, g, :c]
+                assert c >= 1 and (np.diff(row) > 0).all(), "kv_index rows must be strictly ascending"
+                gmask[g, row] = 1
+                if c != kr[g]:
+                    # the prefix masses between the two lengths all lie within the band of p
+                    order = np.lexsort((np.arange(r.m.shape[1]), -r.m[g]))
+                    cum = np.cumsum(r.m[g, order])
+                    lo, hi = min(c, int(kr[g])), max(c, int(kr[g]))
+                    assert np.abs(cum[lo - 1:hi - 1] - r.extra["top_p"]).max() <= band, \
+                        f"P4 kappa_row {c} != {kr[g]} away from the cumulative-mass boundary"
+                    rep["kappa_row_in_band"] = rep.get("kappa_row_in_band", 0) + 1
+                    near[g, order[lo:hi]] = True
         if mask is not None:
             assert (mask[bi, h] == gmask).all(), "mask and kv_index disagree"
         diff = gmask != r.mask
-        near = np.abs(r.m - r.tau[:, None]) <= band
         rep["band_population"] += int(near.sum())
         rep["mask_mismatch"] += int((diff & ~near).sum())
         rep["mask_in_band"] += int((diff & near).sum())
@@ -90,10 +108,12 @@ def oracle_output_with_gpu_selection(q, k, v, sel, B, scale=None, q_blocks=None)
     b, hq = q.shape[0], q.shape[1]
     selections = {}
     pq, pk, idx = sel.perm_q.cpu().numpy(), sel.perm_k.cpu().numpy(), sel.kv_index.cpu().numpy()
+    cnt = sel.kv_count.cpu().numpy()
     grp = hq // k.shape[1]
     for bi in range(b):
         for h in range(hq):
-            selections[(bi, h)] = (pq[bi, h], pk[bi, h // grp], idx[bi, h])
+            rows = [idx[bi, h, g, :cnt[bi, h, g]] for g in range(idx.shape[2])]
+            selections[(bi, h)] = (pq[bi, h], pk[bi, h // grp], rows)
     p = O.Params(block_size=B, scale=scale)
     out, _ = O.ba_attention(q, k, v, p, q_blocks=q_blocks, selections=selections)
     return out

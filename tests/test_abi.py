@@ -101,7 +101,9 @@ def test_sizes_and_kappa(ba):
     (lambda p, pa: setattr(p, "block_size", 32), "UNSUPPORTED"),
     (lambda p, pa: setattr(p, "len_q", 0), "INVALID_ARGUMENT"),
     (lambda p, pa: setattr(pa, "sort", 7), "INVALID_ARGUMENT"),
-    (lambda p, pa: setattr(pa, "select", 1), "UNSUPPORTED"),
+    (lambda p, pa: setattr(pa, "select", 1), "INVALID_ARGUMENT"),          # TOPP with top_p = 0
+    (lambda p, pa: (setattr(pa, "select", 1), setattr(pa, "top_p", 1.01)), "INVALID_ARGUMENT"),
+    (lambda p, pa: setattr(pa, "select", 2), "INVALID_ARGUMENT"),
 ])
 def test_validation_errors(ba, mutate, code):
     q, k, v = _meta(1, 4, 2, 1000, 128)

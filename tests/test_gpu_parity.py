@@ -263,3 +263,50 @@ print("OK", ba.attention_kernel_name(q, k, v, 128))
 """
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=240)
     assert r.returncode == 0 and f"OK {name}\n" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+# ---------------------------------------------------------------- NEXT-1: cumulative-mass budget (reading A23)
+@pytest.mark.parametrize("cfg,L,hq,hkv,B,dens,top_p", [
+    ("T", 1024, 1, 1, 64, 1.0, 0.9),
+    ("A", 4096 + 77, 4, 4, 128, 1.0, 0.5),
+    ("C", 8192, 8, 2, 128, 0.5, 0.95),    # cap binds on flat rows
+    ("M", 4096 + 13, 2, 2, 64, 1.0, 0.99),
+    ("V", 4500, 2, 2, 128, 0.4, 0.7),
+])
+def test_selection_topp(ba, cfg, L, hq, hkv, B, dens, top_p):
+    """TOPP masks and kappa_row vs the oracle (P4 with the cumulative-mass band),
+    then the attention over the variable-length lists (P5)."""
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv)
+    p32 = float(np.float32(top_p))  # the ABI carries top_p as fp32
+    ctx = ba.Context(q, k, v, B, dens, diagnostics=True, top_p=p32)
+    sel = ctx.select(q, k, v)
+    out = torch.empty_like(q)
+    ctx.sparse_attn(out)
+    torch.cuda.synchronize()
+    ref = oracle_select_all(q, k, B, dens, 1.0, "qk", "diag", top_p=p32)
+    check_selection(sel, ref)
+    cnt = sel.kv_count.cpu().numpy()
+    assert (cnt >= 1).all() and (cnt <= sel.kappa).all()
+    tol = TOL[q.dtype]
+    assert max_abs_err(out, oracle_output_with_gpu_selection(q, k, v, sel, B)) <= tol
+
+
+def test_topp_full_mass_keeps_everything(ba):
+    """top_p = 1 with density 1: every row whose mass sums below 1 in fp64
+    keeps all N_k blocks; the rest keep the prefix that reaches 1 — either way
+    the oracle's kappa_row (checked by check_selection)."""
+    w = CONFIGS["A"]
+    q, k, v = make_qkv(w, device="cuda", seq_len=2048, heads_q=2, heads_kv=2)
+    ctx = ba.Context(q, k, v, 128, 1.0, diagnostics=True, top_p=1.0)
+    sel = ctx.select(q, k, v)
+    torch.cuda.synchronize()
+    check_selection(sel, oracle_select_all(q, k, 128, 1.0, 1.0, "qk", "diag", top_p=1.0))
+
+
+def test_topp_rejects_bad_p(ba):
+    w = CONFIGS["A"]
+    q, k, v = make_qkv(w, device="cuda", seq_len=256, heads_q=1, heads_kv=1)
+    for bad in (0.0, 1.5, -0.1):
+        with pytest.raises(ba.BaError, match="INVALID_ARGUMENT"):
+            ba.Context(q, k, v, 128, 0.5, top_p=bad).select(q, k, v)

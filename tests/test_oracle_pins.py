@@ -342,6 +342,61 @@ def test_topk_monotone_in_density():
     assert prev.all()
 
 
+def test_topp_brute_force():
+    """Reading A23: kappa_row is the minimum cardinality of ANY key-block subset
+    whose mass reaches p, and the kept set is a maximum-mass subset of that
+    size (so the greedy prefix is optimal) — brute force over all subsets,
+    N_k <= 9, with and without the density cap."""
+    for _ in range(150):
+        nk = int(RNG.integers(1, 10))
+        m = O.softmax_rows(RNG.normal(size=(1, nk)) * RNG.uniform(0.2, 3.0))
+        p = float(RNG.uniform(0.05, 1.0))
+        cap = int(RNG.integers(1, nk + 1))
+        mask, tau, idx, kap = O.topp_mask(m, p, nk)
+        sizes = [k for k in range(1, nk + 1)
+                 if any(sum(m[0, list(c)]) >= p for c in itertools.combinations(range(nk), k))]
+        kmin = sizes[0] if sizes else nk
+        assert kap[0] == kmin
+        best = max(sum(m[0, list(c)]) for c in itertools.combinations(range(nk), kmin))
+        assert abs(m[0, idx[0]].sum() - best) <= 1e-15
+        assert tau[0] == m[0, idx[0]].min()
+        # capped: the kept set is top-min(kmin, cap) (same order as top-kappa)
+        mask_c, _, idx_c, kap_c = O.topp_mask(m, p, cap)
+        assert kap_c[0] == min(kmin, cap)
+        assert list(idx_c[0]) == list(O.topk_mask(m, int(kap_c[0]))[2][0])
+
+
+def test_topp_closed_forms():
+    """Uniform rows: kappa_row = ceil(p N_k) (the mass of k blocks is k/N_k);
+    p = 1 keeps every block with positive mass; a one-hot-dominant row keeps one
+    block; kappa_row is non-decreasing in p."""
+    for nk in (1, 3, 8, 50):
+        m = np.full((1, nk), 1.0 / nk)
+        for p in (0.1, 0.25, 0.5, 0.77, 1.0):
+            # k/N_k >= p up to the fp64 rounding of the running sum (choose p off the grid)
+            if abs(p * nk - round(p * nk)) < 1e-9:
+                continue
+            _, _, _, kap = O.topp_mask(m, p, nk)
+            assert kap[0] == math.ceil(p * nk)
+    m = np.array([[0.9, 0.05, 0.03, 0.02]])
+    assert O.topp_mask(m, 0.9, 4)[3][0] == 1
+    assert O.topp_mask(m, 0.95, 4)[3][0] == 2
+    assert O.topp_mask(m, 1.0, 4)[3][0] == 4
+    rows = O.softmax_rows(RNG.normal(size=(10, 40)) * 2)
+    prev = np.zeros(10)
+    for p in (0.1, 0.3, 0.5, 0.7, 0.9, 0.99):
+        mask, _, _, kap = O.topp_mask(rows, p, 40)
+        assert (kap >= prev).all() and (mask.sum(1) == kap).all()
+        prev = kap
+
+
+def test_topp_worked(golden):
+    g = golden["topp_a"]
+    mask, tau, idx, kap = O.topp_mask(np.array([g["m"]]), g["top_p"], len(g["m"]))
+    assert list(mask[0]) == g["expected_mask"]
+    assert kap[0] == sum(g["expected_mask"])
+
+
 # ---------------------------------------------------------------- selection special cases
 def test_constant_blocks_pooled_equals_oracle_map():
     """P:388 + Eq. oracle-dist: with constant, equal-size blocks
