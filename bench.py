@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C")
     ap.add_argument("--density", type=float, default=None)
+    ap.add_argument("--top-p", type=float, default=None,
+                    help="cumulative-mass budget (BA_SELECT_TOPP, reading A23) capped at --density")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -62,10 +64,11 @@ def load_peaks():
     return {"tflops_burst": 1590.0, "tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "source": "fallback"}
 
 
-def workload_desc(w, density):
+def workload_desc(w, density, top_p=None):
+    budget = (f"density={density} ({int(round((1 - density) * 100))}% block sparsity)" if top_p is None else
+              f"top_p={top_p} capped at density={density} (cumulative-mass budget)")
     return (f"{w.name} (config {w.config_index}): per rank b=1, Hq={w.heads_q}, Hkv={w.heads_kv}, "
-            f"L={w.seq_len}, d={w.head_dim}, B={w.block_size}, density={density} "
-            f"({int(round((1 - density) * 100))}% block sparsity), sort=qk, comp=diag, beta=1")
+            f"L={w.seq_len}, d={w.head_dim}, B={w.block_size}, {budget}, sort=qk, comp=diag, beta=1")
 
 
 # --------------------------------------------------------------------------- clocks
@@ -237,7 +240,7 @@ def run_ours(args):
         wr = w.with_(config_index=w.config_index + 100 * rank)
         q, k, v = make_qkv(wr, device=dev)
     torch.cuda.synchronize()
-    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag")
+    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag", top_p=args.top_p)
     out = torch.empty_like(q)
     stream = torch.cuda.current_stream()
 
@@ -379,13 +382,14 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if heads else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": workload_desc(w, density), "global_batch": 1 if heads else world,
+            "config": {"workload": workload_desc(w, density, args.top_p), "global_batch": 1 if heads else world,
                        "seq_len": w.seq_len,
                        "parallelism": (f"head-parallel x{world} (whole GQA groups per rank, NCCL all-gather of O)"
                                        if heads else f"batch-parallel x{world} (weak scaling, no data-path collective)"),
                        "l2": "inputs larger than L2 (q+k+v = %.2f GB per step)" %
                              ((q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
-            "roofline": {"bound": "tensor", "kernel": "attn_sm100_tcgen05", "achieved": attn_tflops,
+            "roofline": {"bound": "tensor", "kernel": ba.attention_kernel_name(q, k, v, w.block_size),
+                         "achieved": attn_tflops,
                          "peak": peaks["tflops_sustained"], "unit": "TFLOP/s",
                          "frac": attn_tflops / peaks["tflops_sustained"],
                          "peak_kind": f"{peaks['source']} bf16 sustained (kernel timed inside a long step)",

@@ -59,26 +59,29 @@ def softmax_rows(x) -> np.ndarray:
 # Norm-based ranking — P:436-446 (§3.3), Alg. 1 steps 1-2.
 # --------------------------------------------------------------------------
 def norm_key(X) -> np.ndarray:
-    """Sort key of each row: fp32(||x||_2^2) with the fixed fp64 order of
+    """Sort key of each row: ||x||_2^2 in fp32 with the fixed order of
     reading A4.
 
     P:438 defines the score s_j = ||K_j||_2; sorting by ||x||^2 gives the same
-    order (monotone map).  Reading A4 fixes the arithmetic so that the key is
-    bit-defined: the d features are split into 16 contiguous parts of d/16;
-    each part is summed sequentially in fp64 (x*x is exact in fp64 for bf16 and
-    fp32 inputs); the 16 partial sums are combined by the halving tree
-    p[:8]+p[8:], then [:4]+[4:], [:2]+[2:], [0]+[1]; the result is rounded to
-    fp32 (round-to-nearest-even).  d not divisible by 16 is zero-padded.
+    order (monotone map).  The paper fixes no precision; reading A4 makes the
+    key bit-defined in IEEE fp32 (round-to-nearest-even, no fused multiply-add):
+    the d features are split into 16 contiguous parts of d/16; each part sums
+    x*x sequentially (product rounded, then sum rounded); the 16 partial sums
+    are combined by the halving tree p[:8]+p[8:], then [:4]+[4:], [:2]+[2:],
+    [0]+[1].  d not divisible by 16 is zero-padded.  (The key only ranks rows;
+    its fp32 rounding error, <= 13 u relative, changes nothing but the order of
+    near-equal norms, and both sides round identically.)
     """
-    X = _f64(X)
+    X = _f64(X).astype(np.float32)  # exact: inputs are bf16 / fp32 values
     L, d = X.shape
     if d % 16:  # zero features add exactly 0: pad to a multiple of 16
-        X = np.concatenate([X, np.zeros((L, 16 - d % 16))], axis=1)
+        X = np.concatenate([X, np.zeros((L, 16 - d % 16), dtype=np.float32)], axis=1)
         d = X.shape[1]
     parts = X.reshape(L, 16, d // 16)
-    p = np.zeros((L, 16), dtype=np.float64)
-    for t in range(d // 16):  # sequential within each part
-        p = p + parts[:, :, t] * parts[:, :, t]
+    p = np.zeros((L, 16), dtype=np.float32)
+    for t in range(d // 16):  # sequential within each part, fp32 ops
+        sq = parts[:, :, t] * parts[:, :, t]
+        p = p + sq
     a = p[:, :8] + p[:, 8:]
     a = a[:, :4] + a[:, 4:]
     a = a[:, :2] + a[:, 2:]

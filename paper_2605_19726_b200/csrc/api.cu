@@ -264,11 +264,12 @@ AttnArgs make_attn(const Dims &D, const ba_params *pa) {
   return a;
 }
 
-// B = 128 kernel choice, BA_ATTN_K5 = "pp" (ping-pong pair, attn_sm100_pp.cu),
-// "2cta" (cluster pair, attn_sm100_2cta.cu) or "1cta" (attn_sm100.cu).  The pair
-// kernels walk the union of two adjacent query blocks' lists.
+// B = 128 kernel choice, BA_ATTN_K5 = "pp" (ping-pong pair, attn_sm100_pp.cu; the
+// default: +1.5-2% over 1cta on A and C), "2cta" (cluster pair,
+// attn_sm100_2cta.cu) or "1cta" (attn_sm100.cu).  The pair kernels walk the
+// union of two adjacent query blocks' lists.
 enum K5Kind { K5_1CTA = 0, K5_2CTA = 1, K5_PP = 2 };
-static const int kDefaultK5 = K5_1CTA;
+static const int kDefaultK5 = K5_PP;
 
 static int k5_kind() {
   static int kind = -1;
@@ -289,7 +290,8 @@ bool use_2cta(const AttnArgs &a) { return k5_kind() == K5_2CTA && attn_2cta_supp
 const char *attn_kernel_name(const AttnArgs &a) {
   if (use_pp(a)) return "attn_sm100_tcgen05_pp";
   if (use_2cta(a)) return "attn_sm100_tcgen05_2cta";
-  return attn_sm100_supported(a) ? "attn_sm100_tcgen05" : "attn_simt";
+  if (!attn_sm100_supported(a)) return "attn_simt";
+  return (a.B == 64 && attn_sm100_dual64()) ? "attn_sm100_tcgen05_dual64" : "attn_sm100_tcgen05";
 }
 
 ba_status run_attn(const AttnArgs &a, cudaStream_t st) {

@@ -39,6 +39,7 @@
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -115,10 +116,18 @@ struct UnionWalk {
 // timestamps of the first kTraceTiles tiles for the producers, the MMA issuer
 // and one softmax warp of each half, and prints them.
 constexpr int kTraceTiles = 12;
-template <int kBN, int kEmu, bool kNoSoftmax = false, bool kTrace = false>
+// kDual (B = 64 only, kBN = 128 storage): every 128-key tile is TWO selected
+// 64-key blocks of the union list (entries 2j and 2j+1), so S is a full
+// 128 x 128 MMA (N = 128) instead of two half-width ones; softmax warpgroup hf
+// owns the columns of block 2j+hf, and the row-level max / rescale state is
+// advanced by both warpgroups whenever either block is selected by the rows.
+template <int kBN, int kEmu, bool kNoSoftmax = false, bool kTrace = false, bool kDual = false>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
   using C = Cfg<kBN>;
+  static_assert(!kDual || kBN == 128, "dual tiles use the 128-key storage");
+  constexpr bool kPairQ = C::kPair || kDual;     // a tile = query blocks (2p, 2p+1) of 64 rows
+  constexpr int kBlk = kDual ? 64 : kBN;          // key-block size B
   using Bars = BarsT<C::NKV>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -142,8 +151,8 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
   const int nw = (int)((a.nk + 31) >> 5);
 
   // ---- key-block set of this tile as bitmasks (block A = first query block, B = second for pairs)
-  const int64_t ga = C::kPair ? 2 * (int64_t)tile : tile;
-  const bool has_b = C::kPair && ga + 1 < a.nq;
+  const int64_t ga = kPairQ ? 2 * (int64_t)tile : tile;
+  const bool has_b = kPairQ && ga + 1 < a.nq;
   for (int w = threadIdx.x; w < 2 * kMaskWords; w += kThreads) mask_a[w] = 0u;
   __syncthreads();
   for (int q2 = 0; q2 < (has_b ? 2 : 1); ++q2) {
@@ -171,11 +180,12 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       // a ragged last key block, when selected, is always the last tile of the ascending walk
       const int64_t gl = a.nk - 1;
       const bool sel_last = ((mask_a[gl >> 5] | mask_b[gl >> 5]) >> (gl & 31)) & 1u;
-      bars.last_ragged = sel_last && (a.lk - gl * (int64_t)kBN) < kBN;
+      bars.last_ragged = sel_last && (a.lk - gl * (int64_t)kBlk) < kBlk;
     }
   }
   __syncthreads();
-  const int cnt = (int)bars.n_union;
+  const int n_blk = (int)bars.n_union;                 // selected key blocks (union)
+  const int cnt = kDual ? (n_blk + 1) >> 1 : n_blk;     // key tiles streamed
 
   if (warp == 0 && lane == 0) {
     mbar_init(&bars.q_full, 8);   // one elected arrive per softmax warp
@@ -205,6 +215,8 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       walk.init(mask_a, mask_b);
       for (int j = 0; j < cnt; ++j) {
         const int gk = walk.next();
+        // dual: the second 64-key half; an odd tail reloads gk there (finite data, P = 0 columns)
+        const int gk2 = kDual ? (2 * j + 1 < n_blk ? walk.next() : gk) : gk;
         const int s = j % C::NKV;
         const uint32_t ph = (uint32_t)(j / C::NKV) & 1u;
         mbar_wait(&bars.kv_empty[s], ph ^ 1u);
@@ -215,10 +227,22 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
         }
         const uint32_t dk = base + C::SMEM_KV + s * 2 * C::TILE_BYTES, dv = dk + C::TILE_BYTES;
         mbar_expect_tx(&bars.kv_full[s], 2 * C::TILE_BYTES);
-        tma_load_4d(dk, &tm_k, &bars.kv_full[s], 0, gk * kBN, (int)hk, (int)b);
-        tma_load_4d(dk + C::BOX_BYTES, &tm_k, &bars.kv_full[s], 64, gk * kBN, (int)hk, (int)b);
-        tma_load_4d(dv, &tm_v, &bars.kv_full[s], 0, gk * kBN, (int)hk, (int)b);
-        tma_load_4d(dv + C::BOX_BYTES, &tm_v, &bars.kv_full[s], 64, gk * kBN, (int)hk, (int)b);
+        if constexpr (kDual) {  // 64-row boxes: rows [0,64) <- block gk, rows [64,128) <- block gk2
+          constexpr uint32_t HALF = 64 * 128;  // 64 rows x 128 B inside a 64-column box
+#pragma unroll
+          for (int hb = 0; hb < 2; ++hb) {
+            const int g = hb ? gk2 : gk;
+            tma_load_4d(dk + hb * HALF, &tm_k, &bars.kv_full[s], 0, g * 64, (int)hk, (int)b);
+            tma_load_4d(dk + C::BOX_BYTES + hb * HALF, &tm_k, &bars.kv_full[s], 64, g * 64, (int)hk, (int)b);
+            tma_load_4d(dv + hb * HALF, &tm_v, &bars.kv_full[s], 0, g * 64, (int)hk, (int)b);
+            tma_load_4d(dv + C::BOX_BYTES + hb * HALF, &tm_v, &bars.kv_full[s], 64, g * 64, (int)hk, (int)b);
+          }
+        } else {
+          tma_load_4d(dk, &tm_k, &bars.kv_full[s], 0, gk * kBN, (int)hk, (int)b);
+          tma_load_4d(dk + C::BOX_BYTES, &tm_k, &bars.kv_full[s], 64, gk * kBN, (int)hk, (int)b);
+          tma_load_4d(dv, &tm_v, &bars.kv_full[s], 0, gk * kBN, (int)hk, (int)b);
+          tma_load_4d(dv + C::BOX_BYTES, &tm_v, &bars.kv_full[s], 64, gk * kBN, (int)hk, (int)b);
+        }
       }
     }
     __syncwarp();
@@ -272,7 +296,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
     const int64_t row0 = (int64_t)tile * BM;
     const int nrows = (int)imin64(BM, a.lq - row0);
     // which query block of the tile this warp's rows belong to (pairs: rows 0-63 -> A, 64-127 -> B)
-    const uint32_t *my_mask = (C::kPair && qd >= 2) ? mask_b : mask_a;
+    const uint32_t *my_mask = (kPairQ && qd >= 2) ? mask_b : mask_a;
     // Q row half -> TMEM (A operand of S = Q K^T): element pairs packed per column
     {
       uint32_t qv[32];
@@ -290,17 +314,27 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       if (lane == 0) mbar_arrive(&bars.q_full);
     }
     const float c = a.scale * 1.4426950408889634f;  // scale * log2(e)
-    const int64_t ragged_valid = a.lk - (a.nk - 1) * (int64_t)kBN;  // rows in the last key block
+    const int64_t ragged_valid = a.lk - (a.nk - 1) * (int64_t)kBlk;  // rows in the last key block
     float m = -INFINITY, l = 0.f;
     uint32_t sr[HC];
     const bool last_ragged = bars.last_ragged != 0u;
     UnionWalk walk;  // only pairs need the per-tile block (row-half membership)
-    if constexpr (C::kPair) walk.init(mask_a, mask_b);
+    if constexpr (kPairQ) walk.init(mask_a, mask_b);
     for (int j = 0; j < cnt; ++j) {
-      bool mine = true;
-      if constexpr (C::kPair) {
+      bool mine = true, active = true;  // mine: my columns are selected by my rows; active: any of the tile's
+      bool ragged_here = last_ragged && j == cnt - 1;
+      if constexpr (kDual) {
+        const int g0 = walk.next();
+        const int g1 = 2 * j + 1 < n_blk ? walk.next() : -1;
+        const bool m0 = (my_mask[g0 >> 5] >> (g0 & 31)) & 1u;
+        const bool m1 = g1 >= 0 && ((my_mask[g1 >> 5] >> (g1 & 31)) & 1u);
+        mine = hf ? m1 : m0;
+        active = m0 || m1;
+        ragged_here = last_ragged && (hf ? g1 : g0) == (int)(a.nk - 1);
+      } else if constexpr (C::kPair) {
         const int gk = walk.next();
         mine = (my_mask[gk >> 5] >> (gk & 31)) & 1u;  // warp-uniform
+        active = mine;
       }
       mbar_wait(&bars.s_full[j & 1], (uint32_t)(j >> 1) & 1u);
       if (lane == 0 && qd == 0) TR(5 + 5 * hf, j);
@@ -315,10 +349,10 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
 #pragma unroll
         for (int q2 = 0; q2 < HC / 32; ++q2) tmem_ld_x32(trow + C::s_col(j & 1) + hf * HC + q2 * 32, sr + q2 * 32);
         tmem_wait_ld();
-        if (last_ragged && j == cnt - 1) {
+        if (kDual ? ragged_here : (last_ragged && j == cnt - 1)) {
 #pragma unroll
           for (int i = 0; i < HC; ++i)
-            if (hf * HC + i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
+            if ((kDual ? i : hf * HC + i) >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
         }
       }
       if (lane == 0 && qd == 0) TR(6 + 5 * hf, j);
@@ -340,7 +374,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       named_bar_sync(1 + qd, 64);
       tc_fence_after();
       if (lane == 0 && qd == 0) TR(7 + 5 * hf, j);
-      if (mine) {
+      if (active) {
         const float mt = fmaxf(pmax, red[((j & 1) * 2 + (hf ^ 1)) * 128 + r]) * c;
         if (m == -INFINITY) {
           m = mt;  // first tile of these rows: O rows are still zero (earlier P rows were 0)
@@ -363,6 +397,8 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
             l *= corr;
           }
         }
+      }
+      if (mine) {
         // p = 2^(s*c - m): FFMA2 for the argument, MUFU or polynomial exp2, FADD2 row sums
         const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
@@ -479,23 +515,34 @@ bool make_map(CUtensorMap *m, const void *ptr, int64_t b, int64_t H, int64_t L, 
   return r == CUDA_SUCCESS;
 }
 
-template <int kBN, int kEmu, bool kNoSoftmax, bool kTrace>
+template <int kBN, int kEmu, bool kNoSoftmax, bool kTrace, bool kDual = false>
 cudaError_t launch_variant(const AttnArgs &a, const CUtensorMap &mk, const CUtensorMap &mv, cudaStream_t st) {
   using C = Cfg<kBN>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel<kBN, kEmu, kNoSoftmax, kTrace>,
+    cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel<kBN, kEmu, kNoSoftmax, kTrace, kDual>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int64_t tiles = C::kPair ? (a.nq + 1) / 2 : a.nq;
+  const int64_t tiles = (C::kPair || kDual) ? (a.nq + 1) / 2 : a.nq;
   dim3 grid((unsigned)tiles, (unsigned)(a.batch * a.hq));
-  attn_sm100_kernel<kBN, kEmu, kNoSoftmax, kTrace><<<grid, kThreads, C::SMEM_BYTES, st>>>(a, mk, mv);
+  attn_sm100_kernel<kBN, kEmu, kNoSoftmax, kTrace, kDual><<<grid, kThreads, C::SMEM_BYTES, st>>>(a, mk, mv);
   return cudaGetLastError();
 }
 
 }  // namespace sm100
+
+// B = 64 tile shape: "dual" (default, BA_ATTN_B64 unset) = two 64-key blocks per
+// 128-key MMA tile; BA_ATTN_B64=pair = one 64-key block per (N = 64) tile.
+bool attn_sm100_dual64() {
+  static int v = -1;
+  if (v < 0) {
+    const char *bm = getenv("BA_ATTN_B64");
+    v = (bm && !strcmp(bm, "pair")) ? 0 : 1;
+  }
+  return v == 1;
+}
 
 bool attn_sm100_supported(const AttnArgs &a) {
   return a.dtype == 0 && a.d == 128 && (a.B == 128 || a.B == 64) && a.nk <= 32 * sm100::kMaskWords;
@@ -511,6 +558,7 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
   // exp2 offload fraction: compile-time variants, BA_EXP_EMU=0..2 selects one (tuning knob);
   // BA_ATTN_DEBUG=1 / 2 select the no-softmax / trace profiling variants (B = 128)
   static int emu = -1, dbg = -1;
+  const int b64 = attn_sm100_dual64() ? 1 : 0;
   if (emu < 0) {
     const char *env = getenv("BA_EXP_EMU");
     emu = env ? atoi(env) : kDefaultEmu;
@@ -518,7 +566,16 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
     const char *d = getenv("BA_ATTN_DEBUG");
     dbg = d ? atoi(d) : 0;
   }
-  if (a.B == 64) return launch_variant<64, 0, false, false>(a, mk, mv, st);
+  if (a.B == 64) {
+    if (b64 == 0) return launch_variant<64, 0, false, false>(a, mk, mv, st);
+    if (dbg == 1) {
+      AttnArgs b2 = a;
+      const char *sk = getenv("BA_ATTN_SKIPLOAD");
+      b2.dbg_flags = sk ? atoi(sk) : 0;
+      return launch_variant<128, 0, true, false, true>(b2, mk, mv, st);
+    }
+    return launch_variant<128, 0, false, false, true>(a, mk, mv, st);
+  }
   if (dbg == 1) {
     AttnArgs b2 = a;
     const char *sk = getenv("BA_ATTN_SKIPLOAD");

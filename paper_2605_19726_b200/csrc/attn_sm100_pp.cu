@@ -446,10 +446,10 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
   if (!make_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs, 128) || !make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) ||
       !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128))
     return cudaErrorInvalidValue;
-  static int dbg = -1, emu = -1, stagger = 1;
+  static int dbg = -1, emu = -1, stagger = 0;
   if (dbg < 0) {
     const char *sg = getenv("BA_PP_STAGGER");
-    stagger = sg ? atoi(sg) : 1;
+    stagger = sg ? atoi(sg) : 0;  // measured slower (a lone warp cannot issue MUFU back to back): opt-in
     const char *d = getenv("BA_ATTN_DEBUG");
     dbg = d ? atoi(d) : 0;
     if (dbg < 0 || dbg > 2) dbg = 0;

@@ -76,6 +76,7 @@ struct AttnArgs {
 cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t st);
 cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st);
 bool attn_sm100_supported(const AttnArgs &a);
+bool attn_sm100_dual64();
 cudaError_t launch_attn_2cta(const AttnArgs &a, cudaStream_t st);
 bool attn_2cta_supported(const AttnArgs &a);
 cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st);

@@ -1,9 +1,10 @@
 // select_kernels.cu — BA-Att pattern selection on sm_100a (Alg. 1 steps 1-10,
 // PAPER.md P:535-562).
 //
-//   K1 norm_keys     key = fp32(||x||^2) per Q / K row (reading A4):
-//                    HBM-bound, one half-warp per row, 128-bit loads, fp64
-//                    partial sums combined by an xor-shuffle tree.
+//   K1 norm_keys     key = ||x||^2 in fp32 per Q / K row (reading A4):
+//                    HBM-bound, one half-warp per row, 128-bit loads, fp32
+//                    partial sums (rounded mul, rounded add) combined by an
+//                    xor-shuffle tree.
 //   K2 radix sort    stable ascending argsort of the keys per (batch, head,
 //                    window) segment (ties -> lower index):
 //                    LSD radix, 4 x 8-bit passes, each = tile histogram +
@@ -35,9 +36,11 @@ namespace baatt {
 
 // =====================================================================================
 // K1: norm keys.  One half-warp (16 lanes) per row; lane l owns features
-// [l*d/16, (l+1)*d/16) and sums their squares sequentially in fp64; the 16
+// [l*d/16, (l+1)*d/16) and sums their squares sequentially in fp32; the 16
 // partial sums are combined with xor offsets 8, 4, 2, 1 (a+b == b+a exactly,
-// so every lane of a pair holds the oracle's p[l] + p[l+8], ...).
+// so every lane of a pair holds the oracle's p[l] + p[l+8], ...).  (An fp64
+// sum cost one fp32 -> fp64 conversion per element on the XU pipe: 65% busy,
+// 3.7 TB/s; the fp32 key keeps the kernel on the HBM roofline.)
 // =====================================================================================
 constexpr int kNormRows = 4;  // rows per half-warp: 4 independent 16-byte loads in flight per lane
 
@@ -88,18 +91,16 @@ __global__ void __launch_bounds__(256) norm_keys_kernel(const T *__restrict__ x,
         f[i] = __uint_as_float(w);
       }
     }
-    double s = 0.0;
+    // IEEE fp32, product and sum each rounded (no FMA contraction): reading A4
+    float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < PER_LANE; ++i) {
-      const double v = static_cast<double>(f[i]);
-      s = fma(v, v, s);  // v*v is exact in fp64, so fma == mul-then-add
-    }
-    s += __shfl_xor_sync(0xffffffffu, s, 8);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    for (int i = 0; i < PER_LANE; ++i) s = __fadd_rn(s, __fmul_rn(f[i], f[i]));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 8));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
     if (lane16 == 0 && rows[k] < bh_rows) {
-      const float key = __double2float_rn(s);
+      const float key = s;
       const int64_t o = b * bh_rows + rows[k];
       keys[o] = key;
       if (keys_user) keys_user[o] = key;
@@ -327,8 +328,13 @@ cudaError_t launch_radix_sort(const SortGeom &g, uint32_t *keys_a, uint32_t *val
 // =====================================================================================
 // K3: gather rows through pi and compute per-block mean / population variance.
 // One CTA (256 threads) per (block g, batch*head).  A thread owns one 16-byte
-// chunk (EPC features) of rows r0, r0 + RPI, ...; the block's rows stay in
-// registers between the copy, the mean pass and the variance pass.
+// chunk (EPC features) of rows r0, r0 + RPI, ...: every row load is in flight
+// before the copies are stored.  The moments are ONE pass over the registers
+// with a per-column shift K = the block's first row (exact in fp64):
+//   mean = K + S1/n,  var = S2/n - (S1/n)^2,  S1 = sum (x - K), S2 = sum (x - K)^2
+// — one fp32 -> fp64 conversion per element (the conversions run on the XU pipe,
+// which the two-pass form saturated), and the shift keeps the cancellation at
+// eps * (var + (mean - K)^2) instead of eps * (var + mean^2).
 // =====================================================================================
 template <typename T, int D>
 __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
@@ -339,8 +345,8 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
   constexpr int CPR = D / EPC;       // chunks per row
   constexpr int RPI = 256 / CPR;     // rows per iteration
   constexpr int MAXIT = 128 / RPI;   // B <= 128
-  __shared__ double red[RPI][D + 1];
-  __shared__ double s_mean[D];
+  __shared__ double red[2][RPI][D + 1];
+  __shared__ double s_shift[D];
   const int64_t g = blockIdx.x;
   const int64_t bh = blockIdx.y;  // batch * heads + head
   const int64_t b = bh / heads, h = bh - b * heads;
@@ -370,34 +376,21 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
 #pragma unroll
   for (int it = 0; it < MAXIT; ++it)
     raw[it] = src[it] >= 0 ? ldg16(xbase + (int64_t)src[it] * s2) : make_uint4(0, 0, 0, 0);
-  double acc[EPC];
-#pragma unroll
-  for (int e = 0; e < EPC; ++e) acc[e] = 0.0;
+  uint4 kraw = make_uint4(0, 0, 0, 0);
+  if (mean) kraw = ldg16(xbase + (int64_t)(perm ? __ldg(perm + bh * L + row0) : (int32_t)row0) * s2);  // shift row
 #pragma unroll
   for (int it = 0; it < MAXIT; ++it) {
     const int r = rsub + it * RPI;
-    if (r < n) {
-      stg16(xsbase + (int64_t)r * D, raw[it]);
-      float v[EPC];
-      Chunk<T>::unpack(raw[it], v);
-#pragma unroll
-      for (int e = 0; e < EPC; ++e) acc[e] += (double)v[e];
-    }
+    if (r < n) stg16(xsbase + (int64_t)r * D, raw[it]);
   }
   if (!mean) return;  // V: copy only
+  double kc[EPC], a1[EPC], a2[EPC];
+  {
+    float v[EPC];
+    Chunk<T>::unpack(kraw, v);
 #pragma unroll
-  for (int e = 0; e < EPC; ++e) red[rsub][chunk * EPC + e] = acc[e];
-  __syncthreads();
-  const double inv_n = 1.0 / (double)n;
-  for (int c = threadIdx.x; c < D; c += 256) {
-    double s = 0.0;
-    for (int i = 0; i < RPI; ++i) s += red[i][c];
-    s_mean[c] = s * inv_n;
+    for (int e = 0; e < EPC; ++e) { kc[e] = (double)v[e]; a1[e] = 0.0; a2[e] = 0.0; }
   }
-  __syncthreads();
-  double mu[EPC];
-#pragma unroll
-  for (int e = 0; e < EPC; ++e) { mu[e] = s_mean[chunk * EPC + e]; acc[e] = 0.0; }
 #pragma unroll
   for (int it = 0; it < MAXIT; ++it) {
     const int r = rsub + it * RPI;
@@ -406,21 +399,27 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
       Chunk<T>::unpack(raw[it], v);
 #pragma unroll
       for (int e = 0; e < EPC; ++e) {
-        const double dv = (double)v[e] - mu[e];
-        acc[e] = fma(dv, dv, acc[e]);
+        const double dv = (double)v[e] - kc[e];
+        a1[e] += dv;
+        a2[e] = fma(dv, dv, a2[e]);
       }
     }
   }
-  __syncthreads();
 #pragma unroll
-  for (int e = 0; e < EPC; ++e) red[rsub][chunk * EPC + e] = acc[e];
+  for (int e = 0; e < EPC; ++e) { red[0][rsub][chunk * EPC + e] = a1[e]; red[1][rsub][chunk * EPC + e] = a2[e]; }
+  if (rsub == 0) {
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) s_shift[chunk * EPC + e] = kc[e];
+  }
   __syncthreads();
+  const double inv_n = 1.0 / (double)n;
   const int64_t nb = (L + B - 1) / B;
   for (int c = threadIdx.x; c < D; c += 256) {
-    double s = 0.0;
-    for (int i = 0; i < RPI; ++i) s += red[i][c];
-    mean[(bh * nb + g) * D + c] = s_mean[c];
-    var[(bh * nb + g) * D + c] = s * inv_n;
+    double t1 = 0.0, t2 = 0.0;
+    for (int i = 0; i < RPI; ++i) { t1 += red[0][i][c]; t2 += red[1][i][c]; }
+    const double m1 = t1 * inv_n;
+    mean[(bh * nb + g) * D + c] = s_shift[c] + m1;
+    var[(bh * nb + g) * D + c] = fmax(fma(-m1, m1, t2 * inv_n), 0.0);
   }
 }
 
@@ -441,10 +440,15 @@ cudaError_t launch_gather_stats(int dtype, int d, const void *x, const int64_t *
 // =====================================================================================
 // K4a: compensated block logits as an fp64 micro-GEMM over 3d features.
 // =====================================================================================
-constexpr int kScTile = 128;  // output tile 128 x 128, 256 threads, 8 x 8 per thread
-constexpr int kScK = 8;       // features per smem stage
+constexpr int kScK = 8;  // features per smem stage
 
-template <int D>
+// TILE x TILE output tile, 256 threads as a 16 x 16 grid, (TILE/16)^2 outputs per
+// thread: rows ty + 16 i and columns tx + 16 j — a warp's 16 column threads read
+// 16 consecutive doubles (128 B: every bank once) and its two row groups are
+// broadcasts, so the smem operand reads are conflict-free (the former
+// tx*4 + j mapping put 4 threads on each bank pair).  TILE = 64 for small score
+// maps (config A: 128 tiles of 128 would leave SMs idle).
+template <int D, int TILE>
 __global__ void __launch_bounds__(256) scores_kernel(int64_t hq, int64_t grp, int64_t nq, int64_t nk,
                                                      const double *__restrict__ q_mean,
                                                      const double *__restrict__ q_var,
@@ -452,74 +456,84 @@ __global__ void __launch_bounds__(256) scores_kernel(int64_t hq, int64_t grp, in
                                                      const double *__restrict__ k_var, int comp,
                                                      double inv_sqrt_d, double beta_over_d,
                                                      double *__restrict__ logits) {
-  __shared__ __align__(16) double As[2][kScK][kScTile + 2];
-  __shared__ __align__(16) double Bs[2][kScK][kScTile + 2];
+  constexpr int R = TILE / 16;              // outputs per thread per dim
+  constexpr int LPT = TILE * kScK / 256;    // features each thread loads per operand per stage
+  constexpr int TPR = kScK / LPT;           // loader threads per row
+  __shared__ __align__(16) double As[2][kScK][TILE + 2];
+  __shared__ __align__(16) double Bs[2][kScK][TILE + 2];
   const int64_t bhq = blockIdx.z;            // batch * hq + head
   const int64_t b = bhq / hq, h = bhq - b * hq;
   const int64_t bhk = b * (hq / grp) + h / grp;
-  const int64_t gq0 = (int64_t)blockIdx.y * kScTile, gk0 = (int64_t)blockIdx.x * kScTile;
+  const int64_t gq0 = (int64_t)blockIdx.y * TILE, gk0 = (int64_t)blockIdx.x * TILE;
   const double *qm = q_mean + bhq * nq * D, *qv = q_var + bhq * nq * D;
   const double *km = k_mean + bhk * nk * D, *kv = k_var + bhk * nk * D;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[8][8];
+  double acc[R][R];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < R; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < R; ++j) acc[i][j] = 0.0;
   const int nfeat = comp ? 3 * D : D;
-  // loader: thread -> (row = tid / 2, 4 features); features of part p at column t:
+  // loader: thread -> (row = tid / TPR, LPT features); features of part p at column t:
   //   Xq = [Qbar/sqrt(d), (beta/d) VarQ, (beta/d) Qbar^2],  Xk = [Kbar, Kbar^2 + VarK, VarK]
-  const int lr = threadIdx.x >> 1, lf = (threadIdx.x & 1) * 4;
-  auto load = [&](int c0, int buf) {
+  // Register-staged prefetch: the next stage's global loads are issued before the
+  // current stage's FMAs and stored to smem after them, so their latency is hidden.
+  const int lr = threadIdx.x / TPR, lf = (threadIdx.x % TPR) * LPT;
+  const int64_t gq_l = gq0 + lr, gk_l = gk0 + lr;
+  const bool q_ok = gq_l < nq, k_ok = gk_l < nk;
+  double rqm[LPT], rqv[LPT], rkm[LPT], rkv[LPT];
+  auto fetch = [&](int c0) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < LPT; ++e) {
       const int c = c0 + lf + e;
       const int part = c / D, t = c - part * D;
-      const int64_t gq = gq0 + lr, gk = gk0 + lr;
-      double a = 0.0, bb = 0.0;
-      if (gq < nq) {
-        const double m = qm[gq * D + t];
-        a = part == 0 ? m * inv_sqrt_d : part == 1 ? beta_over_d * qv[gq * D + t] : beta_over_d * (m * m);
-      }
-      if (gk < nk) {
-        const double m = km[gk * D + t];
-        bb = part == 0 ? m : part == 1 ? fma(m, m, kv[gk * D + t]) : kv[gk * D + t];
-      }
-      As[buf][lf + e][lr] = a;
-      Bs[buf][lf + e][lr] = bb;
+      rqm[e] = q_ok ? qm[gq_l * D + t] : 0.0;
+      rqv[e] = (q_ok && part == 1) ? qv[gq_l * D + t] : 0.0;
+      rkm[e] = (k_ok && part < 2) ? km[gk_l * D + t] : 0.0;
+      rkv[e] = (k_ok && part > 0) ? kv[gk_l * D + t] : 0.0;
     }
   };
-  load(0, 0);
+  auto stash = [&](int c0, int buf) {
+#pragma unroll
+    for (int e = 0; e < LPT; ++e) {
+      const int c = c0 + lf + e;
+      const int part = c / D;
+      const double m = rqm[e], k = rkm[e];
+      As[buf][lf + e][lr] = part == 0 ? m * inv_sqrt_d : part == 1 ? beta_over_d * rqv[e] : beta_over_d * (m * m);
+      Bs[buf][lf + e][lr] = part == 0 ? k : part == 1 ? fma(k, k, rkv[e]) : rkv[e];
+    }
+  };
+  fetch(0);
+  stash(0, 0);
   __syncthreads();
   int buf = 0;
   for (int c0 = 0; c0 < nfeat; c0 += kScK) {
-    if (c0 + kScK < nfeat) load(c0 + kScK, buf ^ 1);  // prefetch the next stage
+    const bool more = c0 + kScK < nfeat;
+    if (more) fetch(c0 + kScK);  // loads in flight during the FMAs below
 #pragma unroll
     for (int k = 0; k < kScK; ++k) {
-      double a[8], bb[8];
+      double a[R], bb[R];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        // rows ty*4 .. ty*4+3 and 64 + ty*4 .. : conflict-free 2 x 32-byte reads per operand
-        a[i] = As[buf][k][ty * 4 + i];
-        a[4 + i] = As[buf][k][64 + ty * 4 + i];
-        bb[i] = Bs[buf][k][tx * 4 + i];
-        bb[4 + i] = Bs[buf][k][64 + tx * 4 + i];
+      for (int i = 0; i < R; ++i) {
+        a[i] = As[buf][k][ty + 16 * i];
+        bb[i] = Bs[buf][k][tx + 16 * i];
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < R; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+        for (int j = 0; j < R; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
     }
+    if (more) stash(c0 + kScK, buf ^ 1);
     __syncthreads();
     buf ^= 1;
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t gq = gq0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+  for (int i = 0; i < R; ++i) {
+    const int64_t gq = gq0 + ty + 16 * i;
     if (gq >= nq) continue;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t gk = gk0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+    for (int j = 0; j < R; ++j) {
+      const int64_t gk = gk0 + tx + 16 * j;
       if (gk < nk) logits[(bhq * nq + gq) * nk + gk] = acc[i][j];
     }
   }
@@ -529,14 +543,16 @@ cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t
                           const double *q_mean, const double *q_var, const double *k_mean,
                           const double *k_var, int comp, double beta, double *logits,
                           cudaStream_t st) {
-  dim3 grid((unsigned)((nk + kScTile - 1) / kScTile), (unsigned)((nq + kScTile - 1) / kScTile),
-            (unsigned)(batch * hq));
   const double inv_sqrt_d = 1.0 / sqrt((double)d), bod = beta / (double)d;
   const int64_t grp = hq / hkv;
-  if (d == 128)
-    scores_kernel<128><<<grid, 256, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits);
-  else
-    scores_kernel<64><<<grid, 256, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits);
+  // 128-tiles (4x fewer smem reads per FMA) unless that leaves under ~4 CTAs per SM
+  const int64_t big = ((nk + 127) / 128) * ((nq + 127) / 128) * batch * hq;
+  const int tile = big >= 2 * 148 ? 128 : 64;
+  dim3 grid((unsigned)((nk + tile - 1) / tile), (unsigned)((nq + tile - 1) / tile), (unsigned)(batch * hq));
+#define BA_SC(D, T) scores_kernel<D, T><<<grid, 256, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits)
+  if (d == 128) { if (tile == 128) BA_SC(128, 128); else BA_SC(128, 64); }
+  else { if (tile == 128) BA_SC(64, 128); else BA_SC(64, 64); }
+#undef BA_SC
   return cudaGetLastError();
 }
 

@@ -149,10 +149,13 @@ def test_no_cpu_fallback_without_library(tmp_path):
 
 
 def test_kernel_routing(ba):
-    """bf16, d = 128, B in {64, 128} must run the tcgen05 kernel (never the SIMT path)."""
+    """bf16, d = 128, B in {64, 128} must run a tcgen05 kernel (never the SIMT path):
+    the ping-pong pair kernel for B = 128, the dual-tile kernel for B = 64."""
     q, k, v = _meta(1, 32, 8, 131072, 128)
+    assert ba.attention_kernel_name(q, k, v, 128) == "attn_sm100_tcgen05_pp"
+    q, k, v = _meta(1, 32, 8, 1 << 21, 128)  # N_k > 8192: beyond the pair kernel's bitmask
     assert ba.attention_kernel_name(q, k, v, 128) == "attn_sm100_tcgen05"
     q, k, v = _meta(1, 28, 28, 65536, 128)
-    assert ba.attention_kernel_name(q, k, v, 64) == "attn_sm100_tcgen05"
+    assert ba.attention_kernel_name(q, k, v, 64) == "attn_sm100_tcgen05_dual64"
     q, k, v = _meta(1, 1, 1, 1024, 64, torch.float32)
     assert ba.attention_kernel_name(q, k, v, 64) == "attn_simt"

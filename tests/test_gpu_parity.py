@@ -137,10 +137,13 @@ def test_attention_bf16(ba, cfg, L, hq, hkv, dens):
     assert torch.isfinite(lse).all()
 
 
-def test_attention_bf16_B64(ba):
+@pytest.mark.parametrize("L,dens", [(2048 + 33, 0.5), (64 * 31 + 5, 0.3), (64 * 7, 1.0), (100, 0.5)])
+def test_attention_bf16_B64(ba, L, dens):
+    """B = 64 (dual tiles: two 64-key blocks per 128-key MMA tile), ragged last
+    key/query blocks, odd block counts, full density."""
     w = CONFIGS["M"]
-    q, k, v = make_qkv(w, device="cuda", seq_len=2048 + 33, heads_q=2, heads_kv=2)
-    ctx, sel = _run_select(ba, q, k, v, 64, 0.5)
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=2, heads_kv=2)
+    ctx, sel = _run_select(ba, q, k, v, 64, dens)
     out = torch.empty_like(q)
     ctx.sparse_attn(out)
     torch.cuda.synchronize()
@@ -179,13 +182,14 @@ def test_injected_oracle_mask(ba):
     assert ref_sel  # oracle selection computed on the same inputs
 
 
-@pytest.mark.parametrize("B,k5", [(128, "1cta"), (128, "2cta"), (128, "pp"), (64, "1cta")])
+@pytest.mark.parametrize("B,k5", [(128, "1cta"), (128, "2cta"), (128, "pp"), (64, "dual"), (64, "pair")])
 def test_injected_dissimilar_lists(ba, B, k5):
     """Random (dissimilar) index lists for every query block: exercises the
     pair kernels' union walk where a block skips tiles (P = 0 rows), including
-    a skipped LAST tile (the epilogue must still wait for every PV)."""
+    a skipped LAST tile (the epilogue must still wait for every PV), and for
+    B = 64 odd union lengths (the dual kernel's half-empty last tile)."""
     import subprocess, sys, os
-    env = dict(os.environ, BA_ATTN_K5=k5)
+    env = dict(os.environ, **({"BA_ATTN_K5": k5} if B == 128 else {"BA_ATTN_B64": k5}))
     code = f"""
 import sys; sys.path.insert(0, {os.path.join(os.path.dirname(__file__))!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
 import numpy as np, torch
