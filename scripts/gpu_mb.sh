@@ -1,0 +1,1 @@
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb tools/microbench.cu && /tmp/mb step 2>&1 | tail -8

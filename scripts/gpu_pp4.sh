@@ -1,0 +1,11 @@
+# 4-warpgroup ping-pong kernel: parity (stagger on/off), A/C bench, trace
+for sg in 1 0; do
+BA_PP_STAGGER=$sg timeout 600 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider --timeout 300 -o timeout_method=thread -k "pp4" 2>&1 | tail -2
+done
+BA_ATTN_K5=pp4 BA_PP_STAGGER=1 BA_ATTN_DEBUG=2 timeout 200 python bench.py --config A --steps 1 --warmup 0 --no-e2e --no-cpu --no-dense 2>&1 | grep TRACE | head -12
+for cfg in A C; do
+for mode in "BA_ATTN_K5=pp4 BA_PP_STAGGER=1" "BA_ATTN_K5=pp4 BA_PP_STAGGER=0" "BA_ATTN_K5=pp4 BA_PP_STAGGER=1 BA_EXP_EMU=1" "BA_ATTN_K5=pp4 BA_ATTN_DEBUG=1" "BA_ATTN_K5=pp"; do
+  env $mode timeout 200 python bench.py --config $cfg --steps 5 --warmup 3 --no-e2e --no-cpu --no-dense > gpurun_out/p.json 2>gpurun_out/p.err
+  python -c "import json;d=json.load(open('gpurun_out/p.json'));print('$cfg $mode',d['roofline']['kernel'],'attn',round(d['roofline']['achieved'],1),'value',round(d['value'],1),'clk',(d['clocks'] or {}).get('sm_mhz'),(d['clocks'] or {}).get('reasons'))" 2>&1 | tail -1
+  tail -1 gpurun_out/p.err
+done; done
