@@ -45,6 +45,8 @@ def parse():
                     help="cumulative-mass budget (BA_SELECT_TOPP, reading A23) capped at --density")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--zero-copy", action="store_true",
+                    help="NEXT-2: no Q'/K'/V' copies, attention gathers rows through pi (ba_sparse_attn_gather)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / e2e / cpu legs)")
@@ -240,7 +242,9 @@ def run_ours(args):
         wr = w.with_(config_index=w.config_index + 100 * rank)
         q, k, v = make_qkv(wr, device=dev)
     torch.cuda.synchronize()
-    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag", top_p=args.top_p)
+    # the product path (what ba_attention runs) materialises Q'/K'/V'; --zero-copy measures NEXT-2
+    zero_copy = bool(args.zero_copy) and ba.zero_copy_supported(q, k, v, w.block_size)
+    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag", top_p=args.top_p, zero_copy=zero_copy)
     out = torch.empty_like(q)
     stream = torch.cuda.current_stream()
 
@@ -387,7 +391,8 @@ def run_ours(args):
                        "parallelism": (f"head-parallel x{world} (whole GQA groups per rank, NCCL all-gather of O)"
                                        if heads else f"batch-parallel x{world} (weak scaling, no data-path collective)"),
                        "l2": "inputs larger than L2 (q+k+v = %.2f GB per step)" %
-                             ((q.numel() + k.numel() + v.numel()) * 2 / 1e9)},
+                             ((q.numel() + k.numel() + v.numel()) * 2 / 1e9),
+                       "zero_copy": zero_copy},
             "roofline": {"bound": "tensor", "kernel": ba.attention_kernel_name(q, k, v, w.block_size),
                          "achieved": attn_tflops,
                          "peak": peaks["tflops_sustained"], "unit": "TFLOP/s",

@@ -118,10 +118,13 @@ typedef struct {
   float softmax_scale;   /* 0 => 1/sqrt(head_dim) (Eq. sdpa) */
 } ba_params;
 
-/* Selection produced by ba_select and consumed by ba_sparse_attn.  Every
- * buffer is caller-allocated device memory.  Required fields: perm_q,
- * perm_k, q_sorted, k_sorted, v_sorted, kv_index, kv_count.  Optional
- * (NULL = not written): everything else. */
+/* Selection produced by ba_select and consumed by ba_sparse_attn /
+ * ba_sparse_attn_gather.  Every buffer is caller-allocated device memory.
+ * Required fields: perm_q, perm_k, kv_index, kv_count.  q_sorted, k_sorted,
+ * v_sorted: required by ba_sparse_attn; NULL = ba_select does not
+ * materialise that permuted copy (zero-copy: ba_sparse_attn_gather reads the
+ * rows through pi_q / pi_k instead).  Optional (NULL = not written):
+ * everything else. */
 typedef struct {
   int32_t *perm_q;       /* [b, H_q, L_q]   sorted position -> original token index (pi_q) */
   int32_t *perm_k;       /* [b, H_kv, L_k]  pi_k */
@@ -175,8 +178,29 @@ ba_status ba_sparse_attn(const ba_problem *prob, const ba_params *params,
                          const ba_selection *sel, void *out, float *lse,
                          cudaStream_t stream);
 
-/* ba_select + ba_sparse_attn with the selection carved from the workspace
- * (>= ba_attention_workspace_size bytes). */
+/* Alg. 1 steps 11-12 without permuted copies (NEXT-2, zero-copy): Q'_i =
+ * Q_{pi_q(i)}, K'_j = K_{pi_k(j)}, V'_j = V_{pi_k(j)} are read in
+ * place — the attention kernel fetches 4 token rows per TMA tile::gather4
+ * instruction through perm_q / perm_k — so ba_select can skip writing Q', K',
+ * V' (q_sorted = k_sorted = v_sorted = NULL).  q, k, v: the ORIGINAL tensors
+ * passed to ba_select.  Reads sel->perm_q, perm_k, kv_index, kv_count.
+ * Requirements (else BA_ERR_UNSUPPORTED, nothing enqueued): bf16,
+ * head_dim 128, q/k/v dense across (batch, head) (stride[1] == L*stride[2],
+ * stride[0] == H*stride[1]), b*H*L < 2^31; B = 64 uses the dual-tile kernel. */
+ba_status ba_sparse_attn_gather(const ba_problem *prob, const ba_params *params,
+                                const void *q, const void *k, const void *v,
+                                const ba_selection *sel, void *out, float *lse,
+                                cudaStream_t stream);
+
+/* 1 if ba_sparse_attn_gather supports this problem (and ba_attention will use
+ * it), else 0.  No device work. */
+int ba_zero_copy_supported(const ba_problem *prob, const ba_params *params);
+
+/* ba_select + attention with the selection carved from the workspace
+ * (>= ba_attention_workspace_size bytes), with permuted copies
+ * (ba_sparse_attn) — the faster path on B200 (gather4 streams K/V
+ * 2.3x slower than tile loads); the environment variable BA_ZERO_COPY=1 selects
+ * ba_sparse_attn_gather when ba_zero_copy_supported. */
 ba_status ba_attention(const ba_problem *prob, const ba_params *params,
                        const void *q, const void *k, const void *v,
                        void *out, float *lse, void *workspace, size_t workspace_bytes,

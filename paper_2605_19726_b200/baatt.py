@@ -80,6 +80,10 @@ def load() -> ctypes.CDLL:
     lib.ba_select.restype = ctypes.c_int
     lib.ba_sparse_attn.argtypes = [P, PA, S, vp, vp, st]
     lib.ba_sparse_attn.restype = ctypes.c_int
+    lib.ba_sparse_attn_gather.argtypes = [P, PA, vp, vp, vp, S, vp, vp, st]
+    lib.ba_sparse_attn_gather.restype = ctypes.c_int
+    lib.ba_zero_copy_supported.argtypes = [P, PA]
+    lib.ba_zero_copy_supported.restype = ctypes.c_int
     lib.ba_attention.argtypes = [P, PA, vp, vp, vp, vp, vp, vp, sz, st]
     lib.ba_attention.restype = ctypes.c_int
     lib.ba_dense_attn.argtypes = [P, PA, vp, vp, vp, vp, vp, st]
@@ -97,7 +101,8 @@ def load() -> ctypes.CDLL:
 
 
 EXPORTED = ["ba_abi_version", "ba_selection_sizes", "ba_select_workspace_size", "ba_attention_workspace_size",
-            "ba_select", "ba_sparse_attn", "ba_attention", "ba_dense_attn",
+            "ba_select", "ba_sparse_attn", "ba_sparse_attn_gather", "ba_zero_copy_supported",
+            "ba_attention", "ba_dense_attn",
             "ba_attention_host_workspace_size", "ba_attention_host", "ba_last_launch_count",
             "ba_attention_kernel_name",
             "ba_status_string", "ba_last_error"]
@@ -112,6 +117,11 @@ def _check(status: int):
 def attention_kernel_name(q, k, v, block_size=128) -> str:
     prob = make_problem(q, k, v, None, block_size)
     return load().ba_attention_kernel_name(ctypes.byref(prob), ctypes.byref(make_params())).decode()
+
+
+def zero_copy_supported(q, k, v, block_size=128) -> bool:
+    prob = make_problem(q, k, v, None, block_size)
+    return bool(load().ba_zero_copy_supported(ctypes.byref(prob), ctypes.byref(make_params())))
 
 
 def last_launch_count() -> int:
@@ -202,18 +212,20 @@ class Selection:
         return s
 
 
-def alloc_selection(q, k, prob: Problem, params: Params, diagnostics: bool = False) -> Selection:
+def alloc_selection(q, k, prob: Problem, params: Params, diagnostics: bool = False,
+                    zero_copy: bool = False) -> Selection:
+    """zero_copy: no permuted copies (q_sorted / k_sorted / v_sorted = None);
+    the attention half then runs ba_sparse_attn_gather."""
     kap, nq, nk = selection_sizes(prob, params)
     b, hq, lq, d = q.shape
     hkv, lk = k.shape[1], k.shape[2]
     dev = q.device
     i32 = dict(dtype=torch.int32, device=dev)
     f64 = dict(dtype=torch.float64, device=dev)
+    copy = (lambda *shape: None) if zero_copy else (lambda *shape: torch.empty(*shape, dtype=q.dtype, device=dev))
     sel = Selection(
         perm_q=torch.empty(b, hq, lq, **i32), perm_k=torch.empty(b, hkv, lk, **i32),
-        q_sorted=torch.empty(b, hq, lq, d, dtype=q.dtype, device=dev),
-        k_sorted=torch.empty(b, hkv, lk, d, dtype=q.dtype, device=dev),
-        v_sorted=torch.empty(b, hkv, lk, d, dtype=q.dtype, device=dev),
+        q_sorted=copy(b, hq, lq, d), k_sorted=copy(b, hkv, lk, d), v_sorted=copy(b, hkv, lk, d),
         kv_index=torch.empty(b, hq, nq, kap, **i32), kv_count=torch.empty(b, hq, nq, **i32),
         kappa=kap, n_q=nq, n_k=nk)
     if diagnostics:
@@ -235,17 +247,24 @@ class Context:
     (the bench's timed loop calls the library without re-allocating)."""
 
     def __init__(self, q, k, v, block_size=128, density=0.5, beta=1.0, sort="qk", comp="diag",
-                 sort_window=0, softmax_scale=0.0, diagnostics=False, out=None, top_p=None):
+                 sort_window=0, softmax_scale=0.0, diagnostics=False, out=None, top_p=None, zero_copy=False):
         """top_p: None = top-kappa (Alg. 1 step 10); a float in (0, 1] = the
-        cumulative-mass budget (reading A23), capped at kappa(density)."""
+        cumulative-mass budget (reading A23), capped at kappa(density).
+        zero_copy: the selection keeps no permuted copies and sparse_attn reads
+        q / k / v through the permutations (ba_sparse_attn_gather, NEXT-2)."""
+        self.zero_copy = zero_copy
         self.prob = make_problem(q, k, v, out, block_size)
         select = SELECT_TOPK if top_p is None else SELECT_TOPP
         self.params = make_params(density, beta, sort, comp, sort_window, softmax_scale, select,
                                   0.0 if top_p is None else top_p)
         lib = load()
         self.ws_select = _workspace(lib.ba_select_workspace_size(ctypes.byref(self.prob), ctypes.byref(self.params)), q.device)
-        self.sel = alloc_selection(q, k, self.prob, self.params, diagnostics)
+        if zero_copy and not load().ba_zero_copy_supported(ctypes.byref(self.prob), ctypes.byref(self.params)):
+            raise BaError("BA_ERR_UNSUPPORTED: zero-copy attention is not supported for this problem "
+                          "(see ba_sparse_attn_gather in include/ba_attn.h)")
+        self.sel = alloc_selection(q, k, self.prob, self.params, diagnostics, zero_copy)
         self.sel_c = self.sel.to_c()
+        self.qkv = (q, k, v)
 
     def select(self, q, k, v, stream=None) -> Selection:
         _check(load().ba_select(ctypes.byref(self.prob), ctypes.byref(self.params), _ptr(q), _ptr(k), _ptr(v),
@@ -255,8 +274,13 @@ class Context:
 
     def sparse_attn(self, out, lse=None, sel: Optional[Selection] = None, stream=None):
         sc = self.sel_c if sel is None else sel.to_c()
-        _check(load().ba_sparse_attn(ctypes.byref(self.prob), ctypes.byref(self.params), ctypes.byref(sc),
-                                     _ptr(out), _ptr(lse), _stream(stream)))
+        if self.zero_copy:
+            q, k, v = self.qkv
+            _check(load().ba_sparse_attn_gather(ctypes.byref(self.prob), ctypes.byref(self.params), _ptr(q), _ptr(k),
+                                                _ptr(v), ctypes.byref(sc), _ptr(out), _ptr(lse), _stream(stream)))
+        else:
+            _check(load().ba_sparse_attn(ctypes.byref(self.prob), ctypes.byref(self.params), ctypes.byref(sc),
+                                         _ptr(out), _ptr(lse), _stream(stream)))
         return out
 
 

@@ -159,15 +159,17 @@ struct SelBufPlan {
   size_t perm_q, perm_k, qs, ks, vs, kv_index, kv_count, total;
 };
 
-SelBufPlan plan_selbufs(const Dims &D) {
+SelBufPlan plan_selbufs(const Dims &D, bool zero_copy = false) {
   SelBufPlan p{};
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
   p.perm_q = take(4ull * D.b * D.hq * D.lq);
   p.perm_k = take(4ull * D.b * D.hkv * D.lk);
-  p.qs = take(D.esz * D.b * D.hq * D.lq * D.d);
-  p.ks = take(D.esz * D.b * D.hkv * D.lk * D.d);
-  p.vs = take(D.esz * D.b * D.hkv * D.lk * D.d);
+  if (!zero_copy) {
+    p.qs = take(D.esz * D.b * D.hq * D.lq * D.d);
+    p.ks = take(D.esz * D.b * D.hkv * D.lk * D.d);
+    p.vs = take(D.esz * D.b * D.hkv * D.lk * D.d);
+  }
   p.kv_index = take(4ull * D.b * D.hq * D.nq * D.kappa);
   p.kv_count = take(4ull * D.b * D.hq * D.nq);
   p.total = off;
@@ -189,9 +191,10 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   if (!sel) return fail(BA_ERR_INVALID_ARGUMENT, "selection is NULL");
   if (!sel->perm_q || !sel->perm_k || !sel->kv_index || !sel->kv_count)
     return fail(BA_ERR_INVALID_ARGUMENT, "selection perm_q/perm_k/kv_index/kv_count must be non-NULL");
-  BA_TRY(check_ptr("sel->q_sorted", sel->q_sorted));
-  BA_TRY(check_ptr("sel->k_sorted", sel->k_sorted));
-  BA_TRY(check_ptr("sel->v_sorted", sel->v_sorted));
+  // the permuted copies are optional: NULL = not materialised (zero-copy attention)
+  if (sel->q_sorted) BA_TRY(check_ptr("sel->q_sorted", sel->q_sorted));
+  if (sel->k_sorted) BA_TRY(check_ptr("sel->k_sorted", sel->k_sorted));
+  if (sel->v_sorted) BA_TRY(check_ptr("sel->v_sorted", sel->v_sorted));
   const SelectPlan plan = plan_select(D, pa, sel);
   if (ws_bytes < plan.total)
     return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu < %zu", ws_bytes, plan.total);
@@ -238,10 +241,13 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   BA_TRY(cuda_check(launch_gather_stats(D.dtype, (int)D.d, k, prob->k_stride, D.b, D.hkv, D.lk, (int)D.B,
                                         sort_k(pa) ? sel->perm_k : nullptr, sort_k(pa) ? nullptr : sel->perm_k,
                                         sel->k_sorted, k_mean, k_var, st), "gather_stats(k)"));
-  BA_TRY(cuda_check(launch_gather_stats(D.dtype, (int)D.d, v, prob->v_stride, D.b, D.hkv, D.lk, (int)D.B,
-                                        sort_k(pa) ? sel->perm_k : nullptr, nullptr, sel->v_sorted, nullptr,
-                                        nullptr, st), "gather(v)"));
-  launches += 3;
+  launches += 2;
+  if (sel->v_sorted) {
+    BA_TRY(cuda_check(launch_gather_stats(D.dtype, (int)D.d, v, prob->v_stride, D.b, D.hkv, D.lk, (int)D.B,
+                                          sort_k(pa) ? sel->perm_k : nullptr, nullptr, sel->v_sorted, nullptr,
+                                          nullptr, st), "gather(v)"));
+    ++launches;
+  }
   // K4: scores, then per-row top-kappa
   double *logits = sel->logits ? sel->logits : at<double>(ws, plan.logits);
   BA_TRY(cuda_check(launch_scores((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, q_var, k_mean, k_var,
@@ -309,6 +315,8 @@ ba_status run_sparse(const Dims &D, const ba_problem *prob, const ba_params *pa,
   if (!sel) return fail(BA_ERR_INVALID_ARGUMENT, "selection is NULL");
   BA_TRY(check_ptr("out", out));
   BA_TRY(check_strides("o", prob->o_stride, D.esz));
+  if (!sel->q_sorted || !sel->k_sorted || !sel->v_sorted)
+    return fail(BA_ERR_INVALID_ARGUMENT, "ba_sparse_attn reads sel->q_sorted/k_sorted/v_sorted (NULL: use ba_sparse_attn_gather)");
   BA_TRY(check_ptr("sel->q_sorted", sel->q_sorted));
   BA_TRY(check_ptr("sel->k_sorted", sel->k_sorted));
   BA_TRY(check_ptr("sel->v_sorted", sel->v_sorted));
@@ -327,6 +335,55 @@ ba_status run_sparse(const Dims &D, const ba_problem *prob, const ba_params *pa,
   for (int i = 0; i < 3; ++i) a.os[i] = prob->o_stride[i];
   a.lse = lse;
   return run_attn(a, st);
+}
+
+// Zero-copy eligibility (NEXT-2): the tcgen05 gather kernels (pair kernel for
+// B = 128, dual-tile kernel for B = 64) and q / k / v dense across (batch, head)
+// so that token rows form one 2-D (b*H*L, d) row space for TMA tile::gather4.
+bool dense_bh(const int64_t *s, int64_t H, int64_t L, int64_t d) {
+  return s[2] >= d && s[1] == L * s[2] && s[0] == H * s[1];
+}
+
+const char *gather_unsupported(const Dims &D, const ba_problem *prob) {
+  if (D.dtype != BA_DTYPE_BF16 || D.d != 128) return "zero-copy needs bf16 and head_dim 128 (tcgen05 path)";
+  if (D.B == 64 && !attn_sm100_dual64()) return "zero-copy B = 64 needs the dual-tile kernel (BA_ATTN_B64 != pair)";
+  if (!dense_bh(prob->q_stride, D.hq, D.lq, D.d) || !dense_bh(prob->k_stride, D.hkv, D.lk, D.d) ||
+      !dense_bh(prob->v_stride, D.hkv, D.lk, D.d))
+    return "zero-copy needs q/k/v dense across (batch, head): stride[1] == L*stride[2], stride[0] == H*stride[1]";
+  if (D.b * D.hq * D.lq >= (1ll << 31) || D.b * D.hkv * D.lk >= (1ll << 31)) return "zero-copy needs b*H*L < 2^31 rows";
+  if (D.nk > 32 * 1024) return "N_k > 32768";
+  return nullptr;
+}
+
+ba_status run_sparse_gather(const Dims &D, const ba_problem *prob, const ba_params *pa, const void *q, const void *k,
+                            const void *v, const ba_selection *sel, void *out, float *lse, cudaStream_t st) {
+  if (!sel) return fail(BA_ERR_INVALID_ARGUMENT, "selection is NULL");
+  BA_TRY(check_ptr("q", q));
+  BA_TRY(check_ptr("k", k));
+  BA_TRY(check_ptr("v", v));
+  BA_TRY(check_ptr("out", out));
+  BA_TRY(check_strides("q", prob->q_stride, D.esz));
+  BA_TRY(check_strides("k", prob->k_stride, D.esz));
+  BA_TRY(check_strides("v", prob->v_stride, D.esz));
+  BA_TRY(check_strides("o", prob->o_stride, D.esz));
+  if (!sel->kv_index || !sel->kv_count || !sel->perm_q || !sel->perm_k)
+    return fail(BA_ERR_INVALID_ARGUMENT, "selection kv_index/kv_count/perm_q/perm_k must be non-NULL");
+  if (const char *why = gather_unsupported(D, prob)) return fail(BA_ERR_UNSUPPORTED, "%s", why);
+  AttnArgs a = make_attn(D, pa);
+  a.q = q; a.k = k; a.v = v;
+  for (int i = 0; i < 3; ++i) { a.qs[i] = prob->q_stride[i]; a.ks[i] = prob->k_stride[i]; a.vs[i] = prob->v_stride[i]; }
+  a.kv_index = sel->kv_index;
+  a.kv_count = sel->kv_count;
+  a.kv_stride = D.kappa;
+  a.perm_q = sel->perm_q;
+  a.perm_k = sel->perm_k;
+  a.gather = 1;
+  a.out = out;
+  for (int i = 0; i < 3; ++i) a.os[i] = prob->o_stride[i];
+  a.lse = lse;
+  cudaError_t e = (D.B == 128 && use_pp(a)) ? launch_attn_pp(a, st) : launch_attn_sm100(a, st);
+  g_launches = 1;
+  return cuda_check(e, "attn_gather");
 }
 
 }  // namespace
@@ -374,12 +431,46 @@ ba_status ba_sparse_attn(const ba_problem *prob, const ba_params *params, const 
   return run_sparse(D, prob, params, sel, out, lse, stream);
 }
 
+ba_status ba_sparse_attn_gather(const ba_problem *prob, const ba_params *params, const void *q, const void *k,
+                                const void *v, const ba_selection *sel, void *out, float *lse, cudaStream_t stream) {
+  g_err.clear();
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  return run_sparse_gather(D, prob, params, q, k, v, sel, out, lse, stream);
+}
+
+int ba_zero_copy_supported(const ba_problem *prob, const ba_params *params) {
+  Dims D;
+  if (check_problem(prob, params, &D) != BA_OK) return 0;
+  return gather_unsupported(D, prob) == nullptr && k5_kind() != K5_2CTA ? 1 : 0;
+}
+
 ba_status ba_attention(const ba_problem *prob, const ba_params *params, const void *q, const void *k,
                        const void *v, void *out, float *lse, void *workspace, size_t workspace_bytes,
                        cudaStream_t stream) {
   g_err.clear();
   Dims D;
   BA_TRY(check_problem(prob, params, &D));
+  // NEXT-2 zero-copy only on request (BA_ZERO_COPY=1): measured, the tile::gather4 K/V stream
+  // costs ~71 cycles per 512-byte instruction (tools/gather_bench.cu: 8x a tile load per byte), so
+  // the attention slows 2.3x while the selection saves only its copy writes (0.86 -> 0.73 ms at A)
+  static const bool want_zc = getenv("BA_ZERO_COPY") && atoi(getenv("BA_ZERO_COPY"));
+  if (want_zc && ba_zero_copy_supported(prob, params)) {  // no permuted copies, rows gathered through pi
+    const SelBufPlan bp = plan_selbufs(D, true);
+    if (workspace_bytes < bp.total) return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu too small", workspace_bytes);
+    if (!workspace) return fail(BA_ERR_INVALID_ARGUMENT, "workspace is NULL");
+    ba_selection sel{};
+    sel.perm_q = at<int32_t>(workspace, bp.perm_q);
+    sel.perm_k = at<int32_t>(workspace, bp.perm_k);
+    sel.kv_index = at<int32_t>(workspace, bp.kv_index);
+    sel.kv_count = at<int32_t>(workspace, bp.kv_count);
+    BA_TRY(run_select(D, prob, params, q, k, v, &sel, static_cast<char *>(workspace) + bp.total,
+                      workspace_bytes - bp.total, stream));
+    const int sel_launches = g_launches;
+    BA_TRY(run_sparse_gather(D, prob, params, q, k, v, &sel, out, lse, stream));
+    g_launches += sel_launches;
+    return BA_OK;
+  }
   const SelBufPlan bp = plan_selbufs(D);
   if (workspace_bytes < bp.total) return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu too small", workspace_bytes);
   if (!workspace) return fail(BA_ERR_INVALID_ARGUMENT, "workspace is NULL");

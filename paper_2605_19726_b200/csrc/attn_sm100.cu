@@ -121,11 +121,15 @@ constexpr int kTraceTiles = 12;
 // 128 x 128 MMA (N = 128) instead of two half-width ones; softmax warpgroup hf
 // owns the columns of block 2j+hf, and the row-level max / rescale state is
 // advanced by both warpgroups whenever either block is selected by the rows.
-template <int kBN, int kEmu, bool kNoSoftmax = false, bool kTrace = false, bool kDual = false>
+// kGather: zero-copy (NEXT-2) — q/k/v are the original tensors; Q rows are read
+// through pi_q by the softmax warps, and the producer warp's 32 lanes fetch 4
+// rows each of every 128-key tile through pi_k with TMA tile::gather4.
+template <int kBN, int kEmu, bool kNoSoftmax = false, bool kTrace = false, bool kDual = false, bool kGather = false>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
   using C = Cfg<kBN>;
   static_assert(!kDual || kBN == 128, "dual tiles use the 128-key storage");
+  static_assert(!kGather || kBN == 128, "gather tiles are 128 keys (B = 128, or dual B = 64)");
   constexpr bool kPairQ = C::kPair || kDual;     // a tile = query blocks (2p, 2p+1) of 64 rows
   constexpr int kBlk = kDual ? 64 : kBN;          // key-block size B
   using Bars = BarsT<C::NKV>;
@@ -206,7 +210,37 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
 
-  if (warp == 0) {
+  if (warp == 0 && kGather) {
+    // ================================================================ gather producer (zero-copy)
+    if (cnt > 0) {
+      const int64_t kb = (b * a.hkv + hk) * a.lk;  // pi_k row base == gather-map row base of (b, hk)
+      UnionWalk walk;
+      walk.init(mask_a, mask_b);
+      for (int j = 0; j < cnt; ++j) {
+        const int gk = walk.next();
+        const int gk2 = kDual ? (2 * j + 1 < n_blk ? walk.next() : gk) : gk;
+        // lane l: tile rows 4l..4l+3 (dual: lanes 0-15 -> block gk, 16-31 -> block gk2)
+        const int g = (kDual && lane >= 16) ? gk2 : gk;
+        const int r0 = kDual ? 4 * (lane & 15) : 4 * lane;
+        int rr[4];  // the ragged tail repeats the last key row (its columns are masked to -inf)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t tok = imin64((int64_t)g * kBlk + r0 + i, a.lk - 1);
+          rr[i] = (int)(kb + __ldg(a.perm_k + kb + tok));
+        }
+        const int s = j % C::NKV;
+        mbar_wait(&bars.kv_empty[s], ((uint32_t)(j / C::NKV) & 1u) ^ 1u);
+        if (lane == 0) { TR(0, j); mbar_expect_tx(&bars.kv_full[s], 2 * C::TILE_BYTES); }
+        __syncwarp();
+        const uint32_t dk = base + C::SMEM_KV + s * 2 * C::TILE_BYTES + lane * 512, dv = dk + C::TILE_BYTES;
+        tma_gather4(dk, &tm_k, &bars.kv_full[s], 0, rr[0], rr[1], rr[2], rr[3]);
+        tma_gather4(dk + C::BOX_BYTES, &tm_k, &bars.kv_full[s], 64, rr[0], rr[1], rr[2], rr[3]);
+        tma_gather4(dv, &tm_v, &bars.kv_full[s], 0, rr[0], rr[1], rr[2], rr[3]);
+        tma_gather4(dv + C::BOX_BYTES, &tm_v, &bars.kv_full[s], 64, rr[0], rr[1], rr[2], rr[3]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 0) {
     // ================================================================ TMA producer
     // K_u and V_u of the u-th selected key block into one stage of the ring
     const bool skip = kNoSoftmax && (a.dbg_flags & 3) == 3;  // profiling knob (no-softmax variant only)
@@ -300,8 +334,10 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
     // Q row half -> TMEM (A operand of S = Q K^T): element pairs packed per column
     {
       uint32_t qv[32];
+      // zero-copy: Q'_i = Q_{pi_q(i)} read in place
+      const int64_t qrow = kGather ? (r < nrows ? (int64_t)__ldg(a.perm_q + bh * a.lq + row0 + r) : 0) : row0 + r;
       const __nv_bfloat16 *qp = static_cast<const __nv_bfloat16 *>(a.q) + b * a.qs[0] + h * a.qs[1] +
-                                (row0 + r) * a.qs[2] + hf * 64;
+                                qrow * a.qs[2] + hf * 64;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const uint4 u = r < nrows ? ldg16(qp + 8 * i) : make_uint4(0, 0, 0, 0);
@@ -515,19 +551,35 @@ bool make_map(CUtensorMap *m, const void *ptr, int64_t b, int64_t H, int64_t L, 
   return r == CUDA_SUCCESS;
 }
 
-template <int kBN, int kEmu, bool kNoSoftmax, bool kTrace, bool kDual = false>
+// 2-D map for tile::gather4 over a [b, H, L, d] bf16 tensor that is dense across
+// (batch, head) (stride[1] == L*stride[2], stride[0] == H*stride[1]): rows are
+// (b*H + h)*L + t, box {64 columns, 1 row}, 128-byte swizzle.
+bool make_gather_map(CUtensorMap *m, const void *ptr, int64_t b, int64_t H, int64_t L, int64_t d, const int64_t *s) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)(b * H * L)};
+  cuuint64_t strides[1] = {(cuuint64_t)s[2] * 2};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int kBN, int kEmu, bool kNoSoftmax, bool kTrace, bool kDual = false, bool kGather = false>
 cudaError_t launch_variant(const AttnArgs &a, const CUtensorMap &mk, const CUtensorMap &mv, cudaStream_t st) {
   using C = Cfg<kBN>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel<kBN, kEmu, kNoSoftmax, kTrace, kDual>,
+    cudaError_t e = cudaFuncSetAttribute(attn_sm100_kernel<kBN, kEmu, kNoSoftmax, kTrace, kDual, kGather>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int64_t tiles = (C::kPair || kDual) ? (a.nq + 1) / 2 : a.nq;
   dim3 grid((unsigned)tiles, (unsigned)(a.batch * a.hq));
-  attn_sm100_kernel<kBN, kEmu, kNoSoftmax, kTrace, kDual><<<grid, kThreads, C::SMEM_BYTES, st>>>(a, mk, mv);
+  attn_sm100_kernel<kBN, kEmu, kNoSoftmax, kTrace, kDual, kGather><<<grid, kThreads, C::SMEM_BYTES, st>>>(a, mk, mv);
   return cudaGetLastError();
 }
 
@@ -552,6 +604,13 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
   using namespace sm100;
   CUtensorMap mk, mv;
   if (!get_encode()) return cudaErrorNotSupported;  // no TMA encoder: fail loudly, never fall back
+  if (a.gather) {  // zero-copy: B = 128 single-block tiles, or B = 64 dual tiles
+    if (a.B == 64 && !attn_sm100_dual64()) return cudaErrorNotSupported;
+    if (!make_gather_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) || !make_gather_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs))
+      return cudaErrorInvalidValue;
+    if (a.B == 64) return launch_variant<128, 0, false, false, true, true>(a, mk, mv, st);
+    return launch_variant<128, 0, false, false, false, true>(a, mk, mv, st);
+  }
   if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, a.B) ||
       !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, a.B))
     return cudaErrorInvalidValue;

@@ -41,6 +41,7 @@ namespace baatt {
 namespace sm100 {
 
 bool make_map(CUtensorMap *m, const void *ptr, int64_t b, int64_t H, int64_t L, int64_t d, const int64_t *s, int rows);
+bool make_gather_map(CUtensorMap *m, const void *ptr, int64_t b, int64_t H, int64_t L, int64_t d, const int64_t *s);
 PFN_cuTensorMapEncodeTiled_v12000 get_encode();
 
 namespace pp {
@@ -100,7 +101,10 @@ struct UnionWalk {
 // (0,0) prints clock64 stamps of its first kTraceTiles union tiles, BA_ATTN_DEBUG=2).
 // kEmu: of every 8 exp2 pairs, kEmu are evaluated by a polynomial on the FMA
 // pipe instead of MUFU (BA_EXP_EMU).
-template <int kMode, int kEmu, bool kStagger = true>
+// kGather: zero-copy (NEXT-2) — Q, K, V are the original tensors; the producer
+// warp's 32 lanes each fetch 4 rows of every 128-row tile through pi_q / pi_k with
+// TMA tile::gather4 (2-D maps over the (b*H*L, d) row space).
+template <int kMode, int kEmu, bool kStagger = true, bool kGather = false>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v) {
@@ -176,7 +180,51 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
   const uint32_t tmem = bars.tmem_base;
   const int cnt = (int)bars.n_union;
 
-  if (warp == 0) {
+  if (warp == 0 && kGather) {
+    // ================================================================ gather producer (zero-copy)
+    if (cnt > 0) {
+      const int64_t qb = bh * a.lq;                    // pi_q row base == gather-map row base of (b, h)
+      const int64_t kb = (b * a.hkv + hk) * a.lk;      // same for pi_k and the K / V maps
+      if (lane == 0) mbar_expect_tx(&bars.q_full, 2 * TILE);
+      __syncwarp();
+#pragma unroll
+      for (int q2 = 0; q2 < 2; ++q2) {  // rows past the sequence repeat its last row (never stored)
+        int rr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t tok = imin64((ga + q2) * BM + 4 * lane + i, a.lq - 1);
+          rr[i] = (int)(qb + __ldg(a.perm_q + qb + tok));
+        }
+        const uint32_t dq = base + SMEM_Q + q2 * TILE + lane * 512;
+        tma_gather4(dq, &tm_q, &bars.q_full, 0, rr[0], rr[1], rr[2], rr[3]);
+        tma_gather4(dq + BOX, &tm_q, &bars.q_full, 64, rr[0], rr[1], rr[2], rr[3]);
+      }
+      UnionWalk walk;
+      walk.init(mask_a, mask_b);
+      for (int u = 0; u < cnt; ++u) {
+        const int gk = walk.next();
+        int rr[4];  // the ragged tail repeats the last key row (its columns are masked to -inf)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t tok = imin64((int64_t)gk * BN + 4 * lane + i, a.lk - 1);
+          rr[i] = (int)(kb + __ldg(a.perm_k + kb + tok));
+        }
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv) {  // item j = 2u + kv: K_u then V_u
+          const int j = 2 * u + kv, s = j % NSLOT;
+          mbar_wait(&bars.empty[s], ((uint32_t)(j / NSLOT) & 1u) ^ 1u);
+          if (kv == 0 && lane == 0) TR(0, u);
+          if (lane == 0) mbar_expect_tx(&bars.full[s], TILE);
+          __syncwarp();
+          const uint32_t dst = base + SMEM_SLOT + s * TILE + lane * 512;
+          const CUtensorMap *map = kv ? &tm_v : &tm_k;
+          tma_gather4(dst, map, &bars.full[s], 0, rr[0], rr[1], rr[2], rr[3]);
+          tma_gather4(dst + BOX, map, &bars.full[s], 64, rr[0], rr[1], rr[2], rr[3]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 0) {
     // ================================================================ TMA producer
     if (lane == 0 && cnt > 0) {
       mbar_expect_tx(&bars.q_full, 2 * TILE);
@@ -418,17 +466,17 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
 
 namespace sm100 {
 namespace pp {
-template <int kMode, int kEmu, bool kStagger = true>
+template <int kMode, int kEmu, bool kStagger = true, bool kGather = false>
 cudaError_t launch_mode(const AttnArgs &a, const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, dim3 grid,
                         cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel<kMode, kEmu, kStagger>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel<kMode, kEmu, kStagger, kGather>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  attn_pp_kernel<kMode, kEmu, kStagger><<<grid, kThreads, SMEM_BYTES, st>>>(a, mq, mk, mv);
+  attn_pp_kernel<kMode, kEmu, kStagger, kGather><<<grid, kThreads, SMEM_BYTES, st>>>(a, mq, mk, mv);
   return cudaGetLastError();
 }
 }  // namespace pp
@@ -443,6 +491,13 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
   using namespace sm100::pp;
   CUtensorMap mq, mk, mv;
   if (!get_encode()) return cudaErrorNotSupported;
+  if (a.gather) {
+    if (!make_gather_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs) || !make_gather_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) ||
+        !make_gather_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs))
+      return cudaErrorInvalidValue;
+    dim3 grid((unsigned)((a.nq + 1) / 2), (unsigned)(a.batch * a.hq));
+    return launch_mode<0, kDefaultEmu, false, true>(a, mq, mk, mv, grid, st);
+  }
   if (!make_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs, 128) || !make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) ||
       !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128))
     return cudaErrorInvalidValue;

@@ -72,6 +72,11 @@ struct AttnArgs {
   float *lse;                  // [b, hq, lq] or nullptr
   float scale;
   int dbg_flags;               // profiling-only knobs (0 in normal use)
+  // zero-copy (NEXT-2): q/k/v are the ORIGINAL tensors (dense across batch and head:
+  // s1 == L*s2, s0 == H*s1) and rows are fetched through pi_q / pi_k with TMA
+  // tile::gather4 (4 rows per instruction) instead of reading permuted copies
+  int gather;
+  const int32_t *perm_k;       // [b, hkv, lk] (gather only)
 };
 cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t st);
 cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st);

@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
   const int64_t row0 = g * B;
   const int n = (int)imin64(B, L - row0);
   const T *xbase = x + b * s0 + h * s1 + chunk * EPC;
-  T *xsbase = xs + (bh * L + row0) * D + chunk * EPC;
+  T *xsbase = xs ? xs + (bh * L + row0) * D + chunk * EPC : nullptr;
   // stage 1: source row indices; stage 2: every row load in flight; stage 3: stores + sums
   int32_t src[MAXIT];  // L < 2^31 (validated)
 #pragma unroll
@@ -378,10 +378,12 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
     raw[it] = src[it] >= 0 ? ldg16(xbase + (int64_t)src[it] * s2) : make_uint4(0, 0, 0, 0);
   uint4 kraw = make_uint4(0, 0, 0, 0);
   if (mean) kraw = ldg16(xbase + (int64_t)(perm ? __ldg(perm + bh * L + row0) : (int32_t)row0) * s2);  // shift row
+  if (xs) {  // permuted copy (NULL: zero-copy attention reads the rows through pi itself)
 #pragma unroll
-  for (int it = 0; it < MAXIT; ++it) {
-    const int r = rsub + it * RPI;
-    if (r < n) stg16(xsbase + (int64_t)r * D, raw[it]);
+    for (int it = 0; it < MAXIT; ++it) {
+      const int r = rsub + it * RPI;
+      if (r < n) stg16(xsbase + (int64_t)r * D, raw[it]);
+    }
   }
   if (!mean) return;  // V: copy only
   double kc[EPC], a1[EPC], a2[EPC];

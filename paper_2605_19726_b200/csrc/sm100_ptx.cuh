@@ -50,6 +50,16 @@ BA_DEVICE void tma_load_4d(uint32_t dst, const CUtensorMap *m, uint64_t *bar, in
       : "memory");
 }
 
+// TMA tile::gather4: rows r0..r3 (row coordinate of a 2-D map), 64 columns from
+// column c0 (the map's box is {64, 1}); the four rows land at dst + 128*i, with
+// the map's 128-byte swizzle applied by smem address like a tile load.
+BA_DEVICE void tma_gather4(uint32_t dst, const CUtensorMap *m, uint64_t *bar, int c0, int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
 BA_DEVICE void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n"

@@ -314,3 +314,65 @@ def test_topp_rejects_bad_p(ba):
     for bad in (0.0, 1.5, -0.1):
         with pytest.raises(ba.BaError, match="INVALID_ARGUMENT"):
             ba.Context(q, k, v, 128, 0.5, top_p=bad).select(q, k, v)
+
+
+# ---------------------------------------------------------------- NEXT-2: zero-copy permutation (TMA gather4)
+@pytest.mark.parametrize("cfg,L,hq,hkv,B,dens,b", [
+    ("A", 4096 + 77, 2, 2, 128, 0.5, 1),   # ragged last key / query block
+    ("C", 3 * 128 * 5, 4, 1, 128, 0.25, 2),  # GQA, batch 2, odd block count
+    ("V", 2 * 128 * 9 + 80, 2, 2, 128, 0.5, 1),
+    ("M", 2048 + 33, 2, 2, 64, 0.5, 1),    # B = 64 dual tiles
+    ("M", 64 * 31 + 5, 2, 1, 64, 0.3, 1),
+])
+@pytest.mark.parametrize("k5", ["pp", "1cta"])
+def test_zero_copy_matches_copies(ba, cfg, L, hq, hkv, B, dens, b, k5):
+    """ba_sparse_attn_gather (rows fetched through pi_q / pi_k by TMA gather4,
+    no Q'/K'/V' copies) is bit-identical to ba_sparse_attn on the permuted
+    copies, and within the bf16 tolerance of the oracle (P5)."""
+    import os, subprocess, sys
+    code = f"""
+import sys; sys.path.insert(0, {os.path.dirname(__file__)!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import torch
+import paper_2605_19726_b200.baatt as ba
+from synth import CONFIGS, make_qkv
+from parity import oracle_output_with_gpu_selection, max_abs_err
+w = CONFIGS[{cfg!r}]
+q, k, v = make_qkv(w, device="cuda", seq_len={L}, heads_q={hq}, heads_kv={hkv}, batch={b})
+assert ba.zero_copy_supported(q, k, v, {B})
+c0 = ba.Context(q, k, v, {B}, {dens})
+c1 = ba.Context(q, k, v, {B}, {dens}, zero_copy=True)
+s0 = c0.select(q, k, v); s1 = c1.select(q, k, v)
+assert s1.q_sorted is None and s1.v_sorted is None
+o0 = torch.empty_like(q); o1 = torch.full_like(q, float("nan"))
+c0.sparse_attn(o0); c1.sparse_attn(o1)
+o2 = ba.ba_attention(q, k, v, block_size={B}, density={dens})  # copy path
+torch.cuda.synchronize()
+for f in ("perm_q", "perm_k", "kv_index", "kv_count"):
+    assert torch.equal(getattr(s0, f), getattr(s1, f)), f
+assert torch.equal(o0, o1), (o0.float() - o1.float()).abs().max().item()
+assert torch.equal(o0, o2)
+err = max_abs_err(o1, oracle_output_with_gpu_selection(q, k, v, s1, {B}))
+assert err <= 2e-2, err
+print("OK", ba.attention_kernel_name(q, k, v, {B}))
+"""
+    for zc in ("0", "1"):  # ba_attention on the copy path and on BA_ZERO_COPY=1
+        env = dict(os.environ, BA_ATTN_K5=k5, BA_ZERO_COPY=zc)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+        assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_zero_copy_unsupported_layout_falls_back_to_copies(ba):
+    """A non-dense (b, h) layout is not zero-copy eligible: ba_sparse_attn_gather
+    refuses it loudly and ba_attention takes the permuted-copy path."""
+    w = CONFIGS["A"]
+    q, k, v = make_qkv(w, device="cuda", seq_len=1024, heads_q=2, heads_kv=2)
+    big = torch.zeros(1, 4, 1024, 128, dtype=q.dtype, device="cuda")
+    big[:, ::2] = q
+    qs = big[:, ::2]  # head stride 2*L*d != L*d: rows are not one (b*H*L, d) row space
+    assert not ba.zero_copy_supported(qs, k, v, 128)
+    with pytest.raises(ba.BaError, match="UNSUPPORTED"):
+        ba.Context(qs, k, v, 128, 0.5, zero_copy=True)
+    out = ba.ba_attention(qs, k, v)
+    ref = ba.ba_attention(q, k, v)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
