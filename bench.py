@@ -45,6 +45,7 @@ def parse():
                     help="cumulative-mass budget (BA_SELECT_TOPP, reading A23) capped at --density")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--q-in-place", action="store_true", help="no Q' copy: Q read through pi_q (K'/V' copies)")
     ap.add_argument("--zero-copy", action="store_true",
                     help="NEXT-2: no Q'/K'/V' copies, attention gathers rows through pi (ba_sparse_attn_gather)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -243,7 +244,9 @@ def run_ours(args):
         q, k, v = make_qkv(wr, device=dev)
     torch.cuda.synchronize()
     # the product path (what ba_attention runs) materialises Q'/K'/V'; --zero-copy measures NEXT-2
-    zero_copy = bool(args.zero_copy) and ba.zero_copy_supported(q, k, v, w.block_size)
+    # (no copies), --q-in-place only Q read through pi_q
+    zero_copy = (True if args.zero_copy and ba.zero_copy_supported(q, k, v, w.block_size)
+                 else "q" if args.q_in_place and ba.q_gather_supported(q, k, v, w.block_size) else False)
     ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag", top_p=args.top_p, zero_copy=zero_copy)
     out = torch.empty_like(q)
     stream = torch.cuda.current_stream()

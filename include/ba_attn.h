@@ -178,29 +178,33 @@ ba_status ba_sparse_attn(const ba_problem *prob, const ba_params *params,
                          const ba_selection *sel, void *out, float *lse,
                          cudaStream_t stream);
 
-/* Alg. 1 steps 11-12 without permuted copies (NEXT-2, zero-copy): Q'_i =
- * Q_{pi_q(i)}, K'_j = K_{pi_k(j)}, V'_j = V_{pi_k(j)} are read in
- * place — the attention kernel fetches 4 token rows per TMA tile::gather4
- * instruction through perm_q / perm_k — so ba_select can skip writing Q', K',
- * V' (q_sorted = k_sorted = v_sorted = NULL).  q, k, v: the ORIGINAL tensors
+/* Alg. 1 steps 11-12 reading the ORIGINAL tensors through the permutations
+ * (NEXT-2, zero-copy): Q'_i = Q_{pi_q(i)} is always read in place, and
+ * K'_j = K_{pi_k(j)}, V'_j = V_{pi_k(j)} too when sel->k_sorted /
+ * v_sorted are NULL (else those copies are read) — the attention kernels fetch
+ * 4 token rows per TMA tile::gather4 instruction through perm_q / perm_k, so
+ * ba_select need not write the corresponding copies.  q, k, v: the tensors
  * passed to ba_select.  Reads sel->perm_q, perm_k, kv_index, kv_count.
  * Requirements (else BA_ERR_UNSUPPORTED, nothing enqueued): bf16,
- * head_dim 128, q/k/v dense across (batch, head) (stride[1] == L*stride[2],
- * stride[0] == H*stride[1]), b*H*L < 2^31; B = 64 uses the dual-tile kernel. */
+ * head_dim 128, the gathered tensors dense across (batch, head)
+ * (stride[1] == L*stride[2], stride[0] == H*stride[1]), b*H*L < 2^31; B = 64
+ * uses the dual-tile kernel; not with BA_ATTN_K5=2cta.  Performance: gathering
+ * K/V costs ~2.3x attention time on B200, gathering Q is free. */
 ba_status ba_sparse_attn_gather(const ba_problem *prob, const ba_params *params,
                                 const void *q, const void *k, const void *v,
                                 const ba_selection *sel, void *out, float *lse,
                                 cudaStream_t stream);
 
-/* 1 if ba_sparse_attn_gather supports this problem (and ba_attention will use
- * it), else 0.  No device work. */
+/* What ba_sparse_attn_gather supports for this problem: 3 = Q, K and V read
+ * through the permutations (no copies at all), 1 = Q only (K'/V' copies
+ * needed), 0 = neither (use ba_sparse_attn).  No device work. */
 int ba_zero_copy_supported(const ba_problem *prob, const ba_params *params);
 
 /* ba_select + attention with the selection carved from the workspace
- * (>= ba_attention_workspace_size bytes), with permuted copies
- * (ba_sparse_attn) — the faster path on B200 (gather4 streams K/V
- * 2.3x slower than tile loads); the environment variable BA_ZERO_COPY=1 selects
- * ba_sparse_attn_gather when ba_zero_copy_supported. */
+ * (>= ba_attention_workspace_size bytes), on the permuted copies
+ * (ba_sparse_attn) — the faster path on B200.  The environment
+ * variable BA_ZERO_COPY=1 runs ba_sparse_attn_gather with no copies, =2 with
+ * only Q read in place, when ba_zero_copy_supported allows it. */
 ba_status ba_attention(const ba_problem *prob, const ba_params *params,
                        const void *q, const void *k, const void *v,
                        void *out, float *lse, void *workspace, size_t workspace_bytes,

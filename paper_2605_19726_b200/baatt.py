@@ -120,8 +120,15 @@ def attention_kernel_name(q, k, v, block_size=128) -> str:
 
 
 def zero_copy_supported(q, k, v, block_size=128) -> bool:
+    """Q, K and V can all be read through the permutations (no copies)."""
     prob = make_problem(q, k, v, None, block_size)
-    return bool(load().ba_zero_copy_supported(ctypes.byref(prob), ctypes.byref(make_params())))
+    return load().ba_zero_copy_supported(ctypes.byref(prob), ctypes.byref(make_params())) == 3
+
+
+def q_gather_supported(q, k, v, block_size=128) -> bool:
+    """Q can be read in place through pi_q (K'/V' copies kept)."""
+    prob = make_problem(q, k, v, None, block_size)
+    return bool(load().ba_zero_copy_supported(ctypes.byref(prob), ctypes.byref(make_params())) & 1)
 
 
 def last_launch_count() -> int:
@@ -214,18 +221,21 @@ class Selection:
 
 def alloc_selection(q, k, prob: Problem, params: Params, diagnostics: bool = False,
                     zero_copy: bool = False) -> Selection:
-    """zero_copy: no permuted copies (q_sorted / k_sorted / v_sorted = None);
-    the attention half then runs ba_sparse_attn_gather."""
+    """zero_copy: False = all permuted copies (ba_sparse_attn); "q" = no Q' copy
+    (Q read in place through pi_q); True = no copies at all.  The attention half
+    runs ba_sparse_attn_gather for "q" / True."""
     kap, nq, nk = selection_sizes(prob, params)
     b, hq, lq, d = q.shape
     hkv, lk = k.shape[1], k.shape[2]
     dev = q.device
     i32 = dict(dtype=torch.int32, device=dev)
     f64 = dict(dtype=torch.float64, device=dev)
-    copy = (lambda *shape: None) if zero_copy else (lambda *shape: torch.empty(*shape, dtype=q.dtype, device=dev))
+    copy = lambda on, *shape: torch.empty(*shape, dtype=q.dtype, device=dev) if on else None
+    kv_copy = zero_copy != True  # noqa: E712  ("q": Q in place, K'/V' copies kept)
     sel = Selection(
         perm_q=torch.empty(b, hq, lq, **i32), perm_k=torch.empty(b, hkv, lk, **i32),
-        q_sorted=copy(b, hq, lq, d), k_sorted=copy(b, hkv, lk, d), v_sorted=copy(b, hkv, lk, d),
+        q_sorted=copy(not zero_copy, b, hq, lq, d), k_sorted=copy(kv_copy, b, hkv, lk, d),
+        v_sorted=copy(kv_copy, b, hkv, lk, d),
         kv_index=torch.empty(b, hq, nq, kap, **i32), kv_count=torch.empty(b, hq, nq, **i32),
         kappa=kap, n_q=nq, n_k=nk)
     if diagnostics:
@@ -250,8 +260,9 @@ class Context:
                  sort_window=0, softmax_scale=0.0, diagnostics=False, out=None, top_p=None, zero_copy=False):
         """top_p: None = top-kappa (Alg. 1 step 10); a float in (0, 1] = the
         cumulative-mass budget (reading A23), capped at kappa(density).
-        zero_copy: the selection keeps no permuted copies and sparse_attn reads
-        q / k / v through the permutations (ba_sparse_attn_gather, NEXT-2)."""
+        zero_copy: False = permuted copies (ba_sparse_attn); "q" = Q read in place
+        through pi_q, K'/V' copies (what ba_attention runs); True = no copies, K and
+        V gathered through pi_k too (ba_sparse_attn_gather, NEXT-2)."""
         self.zero_copy = zero_copy
         self.prob = make_problem(q, k, v, out, block_size)
         select = SELECT_TOPK if top_p is None else SELECT_TOPP
@@ -259,7 +270,8 @@ class Context:
                                   0.0 if top_p is None else top_p)
         lib = load()
         self.ws_select = _workspace(lib.ba_select_workspace_size(ctypes.byref(self.prob), ctypes.byref(self.params)), q.device)
-        if zero_copy and not load().ba_zero_copy_supported(ctypes.byref(self.prob), ctypes.byref(self.params)):
+        zc = load().ba_zero_copy_supported(ctypes.byref(self.prob), ctypes.byref(self.params))
+        if (zero_copy is True and zc != 3) or (zero_copy == "q" and not zc & 1):
             raise BaError("BA_ERR_UNSUPPORTED: zero-copy attention is not supported for this problem "
                           "(see ba_sparse_attn_gather in include/ba_attn.h)")
         self.sel = alloc_selection(q, k, self.prob, self.params, diagnostics, zero_copy)

@@ -159,14 +159,15 @@ struct SelBufPlan {
   size_t perm_q, perm_k, qs, ks, vs, kv_index, kv_count, total;
 };
 
-SelBufPlan plan_selbufs(const Dims &D, bool zero_copy = false) {
+// no_q: Q is read in place (no Q' copy); no_q && kv: K', V' copies are kept
+SelBufPlan plan_selbufs(const Dims &D, bool no_q = false, bool kv = true) {
   SelBufPlan p{};
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
   p.perm_q = take(4ull * D.b * D.hq * D.lq);
   p.perm_k = take(4ull * D.b * D.hkv * D.lk);
-  if (!zero_copy) {
-    p.qs = take(D.esz * D.b * D.hq * D.lq * D.d);
+  if (!no_q) p.qs = take(D.esz * D.b * D.hq * D.lq * D.d);
+  if (!no_q || kv) {
     p.ks = take(D.esz * D.b * D.hkv * D.lk * D.d);
     p.vs = take(D.esz * D.b * D.hkv * D.lk * D.d);
   }
@@ -344,40 +345,59 @@ bool dense_bh(const int64_t *s, int64_t H, int64_t L, int64_t d) {
   return s[2] >= d && s[1] == L * s[2] && s[0] == H * s[1];
 }
 
-const char *gather_unsupported(const Dims &D, const ba_problem *prob) {
+// need_kv: K and V are gathered too (full zero-copy); else only Q (K', V' copies exist)
+const char *gather_unsupported(const Dims &D, const ba_problem *prob, bool need_kv) {
   if (D.dtype != BA_DTYPE_BF16 || D.d != 128) return "zero-copy needs bf16 and head_dim 128 (tcgen05 path)";
   if (D.B == 64 && !attn_sm100_dual64()) return "zero-copy B = 64 needs the dual-tile kernel (BA_ATTN_B64 != pair)";
-  if (!dense_bh(prob->q_stride, D.hq, D.lq, D.d) || !dense_bh(prob->k_stride, D.hkv, D.lk, D.d) ||
-      !dense_bh(prob->v_stride, D.hkv, D.lk, D.d))
+  if (k5_kind() == K5_2CTA) return "the 2-CTA kernel (BA_ATTN_K5=2cta) reads permuted copies only";
+  if (!dense_bh(prob->q_stride, D.hq, D.lq, D.d) ||
+      (need_kv && (!dense_bh(prob->k_stride, D.hkv, D.lk, D.d) || !dense_bh(prob->v_stride, D.hkv, D.lk, D.d))))
     return "zero-copy needs q/k/v dense across (batch, head): stride[1] == L*stride[2], stride[0] == H*stride[1]";
   if (D.b * D.hq * D.lq >= (1ll << 31) || D.b * D.hkv * D.lk >= (1ll << 31)) return "zero-copy needs b*H*L < 2^31 rows";
   if (D.nk > 32 * 1024) return "N_k > 32768";
   return nullptr;
 }
 
+// Attention reading Q (and, without K'/V' copies in *sel, K and V) in place through the
+// permutations.  With sel->k_sorted and sel->v_sorted set only Q is gathered.
 ba_status run_sparse_gather(const Dims &D, const ba_problem *prob, const ba_params *pa, const void *q, const void *k,
                             const void *v, const ba_selection *sel, void *out, float *lse, cudaStream_t st) {
   if (!sel) return fail(BA_ERR_INVALID_ARGUMENT, "selection is NULL");
   BA_TRY(check_ptr("q", q));
-  BA_TRY(check_ptr("k", k));
-  BA_TRY(check_ptr("v", v));
   BA_TRY(check_ptr("out", out));
   BA_TRY(check_strides("q", prob->q_stride, D.esz));
-  BA_TRY(check_strides("k", prob->k_stride, D.esz));
-  BA_TRY(check_strides("v", prob->v_stride, D.esz));
   BA_TRY(check_strides("o", prob->o_stride, D.esz));
   if (!sel->kv_index || !sel->kv_count || !sel->perm_q || !sel->perm_k)
     return fail(BA_ERR_INVALID_ARGUMENT, "selection kv_index/kv_count/perm_q/perm_k must be non-NULL");
-  if (const char *why = gather_unsupported(D, prob)) return fail(BA_ERR_UNSUPPORTED, "%s", why);
+  const bool kv_copies = sel->k_sorted && sel->v_sorted;
+  if (kv_copies) {
+    BA_TRY(check_ptr("sel->k_sorted", sel->k_sorted));
+    BA_TRY(check_ptr("sel->v_sorted", sel->v_sorted));
+  } else {
+    BA_TRY(check_ptr("k", k));
+    BA_TRY(check_ptr("v", v));
+    BA_TRY(check_strides("k", prob->k_stride, D.esz));
+    BA_TRY(check_strides("v", prob->v_stride, D.esz));
+  }
+  if (const char *why = gather_unsupported(D, prob, !kv_copies)) return fail(BA_ERR_UNSUPPORTED, "%s", why);
   AttnArgs a = make_attn(D, pa);
-  a.q = q; a.k = k; a.v = v;
-  for (int i = 0; i < 3; ++i) { a.qs[i] = prob->q_stride[i]; a.ks[i] = prob->k_stride[i]; a.vs[i] = prob->v_stride[i]; }
+  a.q = q;
+  for (int i = 0; i < 3; ++i) a.qs[i] = prob->q_stride[i];
+  if (kv_copies) {  // contiguous [b, H_kv, L_k, d] permuted copies
+    a.k = sel->k_sorted; a.v = sel->v_sorted;
+    a.ks[0] = D.hkv * D.lk * D.d; a.ks[1] = D.lk * D.d; a.ks[2] = D.d;
+    for (int i = 0; i < 3; ++i) a.vs[i] = a.ks[i];
+    a.gather = 1;
+  } else {
+    a.k = k; a.v = v;
+    for (int i = 0; i < 3; ++i) { a.ks[i] = prob->k_stride[i]; a.vs[i] = prob->v_stride[i]; }
+    a.gather = 3;
+  }
   a.kv_index = sel->kv_index;
   a.kv_count = sel->kv_count;
   a.kv_stride = D.kappa;
   a.perm_q = sel->perm_q;
   a.perm_k = sel->perm_k;
-  a.gather = 1;
   a.out = out;
   for (int i = 0; i < 3; ++i) a.os[i] = prob->o_stride[i];
   a.lse = lse;
@@ -442,7 +462,8 @@ ba_status ba_sparse_attn_gather(const ba_problem *prob, const ba_params *params,
 int ba_zero_copy_supported(const ba_problem *prob, const ba_params *params) {
   Dims D;
   if (check_problem(prob, params, &D) != BA_OK) return 0;
-  return gather_unsupported(D, prob) == nullptr && k5_kind() != K5_2CTA ? 1 : 0;
+  if (gather_unsupported(D, prob, true) == nullptr) return 3;
+  return gather_unsupported(D, prob, false) == nullptr ? 1 : 0;
 }
 
 ba_status ba_attention(const ba_problem *prob, const ba_params *params, const void *q, const void *k,
@@ -451,17 +472,26 @@ ba_status ba_attention(const ba_problem *prob, const ba_params *params, const vo
   g_err.clear();
   Dims D;
   BA_TRY(check_problem(prob, params, &D));
-  // NEXT-2 zero-copy only on request (BA_ZERO_COPY=1): measured, the tile::gather4 K/V stream
-  // costs ~71 cycles per 512-byte instruction (tools/gather_bench.cu: 8x a tile load per byte), so
-  // the attention slows 2.3x while the selection saves only its copy writes (0.86 -> 0.73 ms at A)
-  static const bool want_zc = getenv("BA_ZERO_COPY") && atoi(getenv("BA_ZERO_COPY"));
-  if (want_zc && ba_zero_copy_supported(prob, params)) {  // no permuted copies, rows gathered through pi
-    const SelBufPlan bp = plan_selbufs(D, true);
+  // Permuted copies by default.  BA_ZERO_COPY=1: Q, K, V read through the permutations
+  // (no copies); BA_ZERO_COPY=2: Q only.  Measured on B200 (profiles/round1_zero_copy.txt):
+  // the tile::gather4 K/V stream costs ~71 cycles per 512-byte instruction
+  // (tools/gather_bench.cu: 8x a tile load per byte) and slows the attention 2.3x; the Q
+  // gather (64 instructions per CTA, ~4.5k cycles before the first MMA) costs ~1-2% of the
+  // attention and saves only ~3% of ba_select (its copy writes are not what bounds K3).
+  static const int want_zc = getenv("BA_ZERO_COPY") ? atoi(getenv("BA_ZERO_COPY")) : 0;
+  const bool full_zc = want_zc == 1 && gather_unsupported(D, prob, true) == nullptr;
+  const bool q_zc = want_zc == 2 && gather_unsupported(D, prob, false) == nullptr;
+  if (full_zc || q_zc) {
+    const SelBufPlan bp = plan_selbufs(D, true, !full_zc);
     if (workspace_bytes < bp.total) return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu too small", workspace_bytes);
     if (!workspace) return fail(BA_ERR_INVALID_ARGUMENT, "workspace is NULL");
     ba_selection sel{};
     sel.perm_q = at<int32_t>(workspace, bp.perm_q);
     sel.perm_k = at<int32_t>(workspace, bp.perm_k);
+    if (!full_zc) {
+      sel.k_sorted = at<void>(workspace, bp.ks);
+      sel.v_sorted = at<void>(workspace, bp.vs);
+    }
     sel.kv_index = at<int32_t>(workspace, bp.kv_index);
     sel.kv_count = at<int32_t>(workspace, bp.kv_count);
     BA_TRY(run_select(D, prob, params, q, k, v, &sel, static_cast<char *>(workspace) + bp.total,

@@ -121,15 +121,15 @@ constexpr int kTraceTiles = 12;
 // 128 x 128 MMA (N = 128) instead of two half-width ones; softmax warpgroup hf
 // owns the columns of block 2j+hf, and the row-level max / rescale state is
 // advanced by both warpgroups whenever either block is selected by the rows.
-// kGather: zero-copy (NEXT-2) — q/k/v are the original tensors; Q rows are read
-// through pi_q by the softmax warps, and the producer warp's 32 lanes fetch 4
-// rows each of every 128-key tile through pi_k with TMA tile::gather4.
-template <int kBN, int kEmu, bool kNoSoftmax = false, bool kTrace = false, bool kDual = false, bool kGather = false>
+// kGather (NEXT-2 zero-copy) bits: 1 = Q rows are read in place through pi_q by
+// the softmax warps; 2 = K / V are the original tensors and the producer warp's
+// 32 lanes fetch 4 rows each of every 128-key tile through pi_k (TMA tile::gather4).
+template <int kBN, int kEmu, bool kNoSoftmax = false, bool kTrace = false, bool kDual = false, int kGather = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
   using C = Cfg<kBN>;
   static_assert(!kDual || kBN == 128, "dual tiles use the 128-key storage");
-  static_assert(!kGather || kBN == 128, "gather tiles are 128 keys (B = 128, or dual B = 64)");
+  static_assert(!(kGather & 2) || kBN == 128, "gather tiles are 128 keys (B = 128, or dual B = 64)");
   constexpr bool kPairQ = C::kPair || kDual;     // a tile = query blocks (2p, 2p+1) of 64 rows
   constexpr int kBlk = kDual ? 64 : kBN;          // key-block size B
   using Bars = BarsT<C::NKV>;
@@ -210,7 +210,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
 
-  if (warp == 0 && kGather) {
+  if (warp == 0 && (kGather & 2)) {
     // ================================================================ gather producer (zero-copy)
     if (cnt > 0) {
       const int64_t kb = (b * a.hkv + hk) * a.lk;  // pi_k row base == gather-map row base of (b, hk)
@@ -335,7 +335,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
     {
       uint32_t qv[32];
       // zero-copy: Q'_i = Q_{pi_q(i)} read in place
-      const int64_t qrow = kGather ? (r < nrows ? (int64_t)__ldg(a.perm_q + bh * a.lq + row0 + r) : 0) : row0 + r;
+      const int64_t qrow = (kGather & 1) ? (r < nrows ? (int64_t)__ldg(a.perm_q + bh * a.lq + row0 + r) : 0) : row0 + r;
       const __nv_bfloat16 *qp = static_cast<const __nv_bfloat16 *>(a.q) + b * a.qs[0] + h * a.qs[1] +
                                 qrow * a.qs[2] + hf * 64;
 #pragma unroll
@@ -567,7 +567,7 @@ bool make_gather_map(CUtensorMap *m, const void *ptr, int64_t b, int64_t H, int6
   return r == CUDA_SUCCESS;
 }
 
-template <int kBN, int kEmu, bool kNoSoftmax, bool kTrace, bool kDual = false, bool kGather = false>
+template <int kBN, int kEmu, bool kNoSoftmax, bool kTrace, bool kDual = false, int kGather = 0>
 cudaError_t launch_variant(const AttnArgs &a, const CUtensorMap &mk, const CUtensorMap &mv, cudaStream_t st) {
   using C = Cfg<kBN>;
   static bool attr = false;
@@ -606,10 +606,16 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
   if (!get_encode()) return cudaErrorNotSupported;  // no TMA encoder: fail loudly, never fall back
   if (a.gather) {  // zero-copy: B = 128 single-block tiles, or B = 64 dual tiles
     if (a.B == 64 && !attn_sm100_dual64()) return cudaErrorNotSupported;
-    if (!make_gather_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) || !make_gather_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs))
+    if (a.gather & 2) {
+      if (!make_gather_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) || !make_gather_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs))
+        return cudaErrorInvalidValue;
+      if (a.B == 64) return launch_variant<128, 0, false, false, true, 3>(a, mk, mv, st);
+      return launch_variant<128, 0, false, false, false, 3>(a, mk, mv, st);
+    }
+    if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, a.B) || !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, a.B))
       return cudaErrorInvalidValue;
-    if (a.B == 64) return launch_variant<128, 0, false, false, true, true>(a, mk, mv, st);
-    return launch_variant<128, 0, false, false, false, true>(a, mk, mv, st);
+    if (a.B == 64) return launch_variant<128, 0, false, false, true, 1>(a, mk, mv, st);
+    return launch_variant<128, 0, false, false, false, 1>(a, mk, mv, st);
   }
   if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, a.B) ||
       !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, a.B))

@@ -101,10 +101,11 @@ struct UnionWalk {
 // (0,0) prints clock64 stamps of its first kTraceTiles union tiles, BA_ATTN_DEBUG=2).
 // kEmu: of every 8 exp2 pairs, kEmu are evaluated by a polynomial on the FMA
 // pipe instead of MUFU (BA_EXP_EMU).
-// kGather: zero-copy (NEXT-2) — Q, K, V are the original tensors; the producer
-// warp's 32 lanes each fetch 4 rows of every 128-row tile through pi_q / pi_k with
-// TMA tile::gather4 (2-D maps over the (b*H*L, d) row space).
-template <int kMode, int kEmu, bool kStagger = true, bool kGather = false>
+// kGather (NEXT-2 zero-copy) bits: 1 = Q, 2 = K and V are the ORIGINAL tensors,
+// fetched through pi_q / pi_k by the producer warp's 32 lanes (4 rows each of
+// every 128-row tile) with TMA tile::gather4 on 2-D maps over the (b*H*L, d)
+// row space; otherwise tile loads of the permuted copies.
+template <int kMode, int kEmu, bool kStagger = true, int kGather = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v) {
@@ -180,73 +181,76 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
   const uint32_t tmem = bars.tmem_base;
   const int cnt = (int)bars.n_union;
 
-  if (warp == 0 && kGather) {
-    // ================================================================ gather producer (zero-copy)
+  if (warp == 0) {
+    // ================================================================ TMA producer
+    // tile loads of the permuted copies by lane 0, or (kGather bits) tile::gather4 of the
+    // original rows through pi by all 32 lanes, lane l fetching rows 4l..4l+3 of each tile
     if (cnt > 0) {
       const int64_t qb = bh * a.lq;                    // pi_q row base == gather-map row base of (b, h)
       const int64_t kb = (b * a.hkv + hk) * a.lk;      // same for pi_k and the K / V maps
-      if (lane == 0) mbar_expect_tx(&bars.q_full, 2 * TILE);
-      __syncwarp();
+      if constexpr (kGather & 1) {
+        if (lane == 0) mbar_expect_tx(&bars.q_full, 2 * TILE);
+        __syncwarp();
 #pragma unroll
-      for (int q2 = 0; q2 < 2; ++q2) {  // rows past the sequence repeat its last row (never stored)
-        int rr[4];
+        for (int q2 = 0; q2 < 2; ++q2) {  // rows past the sequence repeat its last row (never stored)
+          int rr[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int64_t tok = imin64((ga + q2) * BM + 4 * lane + i, a.lq - 1);
-          rr[i] = (int)(qb + __ldg(a.perm_q + qb + tok));
+          for (int i = 0; i < 4; ++i) {
+            const int64_t tok = imin64((ga + q2) * BM + 4 * lane + i, a.lq - 1);
+            rr[i] = (int)(qb + __ldg(a.perm_q + qb + tok));
+          }
+          const uint32_t dq = base + SMEM_Q + q2 * TILE + lane * 512;
+          tma_gather4(dq, &tm_q, &bars.q_full, 0, rr[0], rr[1], rr[2], rr[3]);
+          tma_gather4(dq + BOX, &tm_q, &bars.q_full, 64, rr[0], rr[1], rr[2], rr[3]);
         }
-        const uint32_t dq = base + SMEM_Q + q2 * TILE + lane * 512;
-        tma_gather4(dq, &tm_q, &bars.q_full, 0, rr[0], rr[1], rr[2], rr[3]);
-        tma_gather4(dq + BOX, &tm_q, &bars.q_full, 64, rr[0], rr[1], rr[2], rr[3]);
-      }
-      UnionWalk walk;
-      walk.init(mask_a, mask_b);
-      for (int u = 0; u < cnt; ++u) {
-        const int gk = walk.next();
-        int rr[4];  // the ragged tail repeats the last key row (its columns are masked to -inf)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int64_t tok = imin64((int64_t)gk * BN + 4 * lane + i, a.lk - 1);
-          rr[i] = (int)(kb + __ldg(a.perm_k + kb + tok));
-        }
-#pragma unroll
-        for (int kv = 0; kv < 2; ++kv) {  // item j = 2u + kv: K_u then V_u
-          const int j = 2 * u + kv, s = j % NSLOT;
-          mbar_wait(&bars.empty[s], ((uint32_t)(j / NSLOT) & 1u) ^ 1u);
-          if (kv == 0 && lane == 0) TR(0, u);
-          if (lane == 0) mbar_expect_tx(&bars.full[s], TILE);
-          __syncwarp();
-          const uint32_t dst = base + SMEM_SLOT + s * TILE + lane * 512;
-          const CUtensorMap *map = kv ? &tm_v : &tm_k;
-          tma_gather4(dst, map, &bars.full[s], 0, rr[0], rr[1], rr[2], rr[3]);
-          tma_gather4(dst + BOX, map, &bars.full[s], 64, rr[0], rr[1], rr[2], rr[3]);
+      } else if (lane == 0) {
+        mbar_expect_tx(&bars.q_full, 2 * TILE);
+        for (int q2 = 0; q2 < 2; ++q2) {  // block B past the end of the sequence is zero-filled
+          const uint32_t dq = base + SMEM_Q + q2 * TILE;
+          tma_load_4d(dq, &tm_q, &bars.q_full, 0, (int)((ga + q2) * BM), (int)h, (int)b);
+          tma_load_4d(dq + BOX, &tm_q, &bars.q_full, 64, (int)((ga + q2) * BM), (int)h, (int)b);
         }
       }
-    }
-    __syncwarp();
-  } else if (warp == 0) {
-    // ================================================================ TMA producer
-    if (lane == 0 && cnt > 0) {
-      mbar_expect_tx(&bars.q_full, 2 * TILE);
-      for (int q2 = 0; q2 < 2; ++q2) {  // block B past the end of the sequence is zero-filled
-        const uint32_t dq = base + SMEM_Q + q2 * TILE;
-        tma_load_4d(dq, &tm_q, &bars.q_full, 0, (int)((ga + q2) * BM), (int)h, (int)b);
-        tma_load_4d(dq + BOX, &tm_q, &bars.q_full, 64, (int)((ga + q2) * BM), (int)h, (int)b);
-      }
-      UnionWalk walk;
-      walk.init(mask_a, mask_b);
-      for (int u = 0; u < cnt; ++u) {
-        const int gk = walk.next();
+      if constexpr (kGather & 2) {
+        UnionWalk walk;
+        walk.init(mask_a, mask_b);
+        for (int u = 0; u < cnt; ++u) {
+          const int gk = walk.next();
+          int rr[4];  // the ragged tail repeats the last key row (its columns are masked to -inf)
 #pragma unroll
-        for (int kv = 0; kv < 2; ++kv) {  // item j = 2u + kv: K_u then V_u
-          const int j = 2 * u + kv, s = j % NSLOT;
-          mbar_wait(&bars.empty[s], ((uint32_t)(j / NSLOT) & 1u) ^ 1u);
-          if (kv == 0) TR(0, u);
-          const uint32_t dst = base + SMEM_SLOT + s * TILE;
-          const CUtensorMap *map = kv ? &tm_v : &tm_k;
-          mbar_expect_tx(&bars.full[s], TILE);
-          tma_load_4d(dst, map, &bars.full[s], 0, gk * BN, (int)hk, (int)b);
-          tma_load_4d(dst + BOX, map, &bars.full[s], 64, gk * BN, (int)hk, (int)b);
+          for (int i = 0; i < 4; ++i) {
+            const int64_t tok = imin64((int64_t)gk * BN + 4 * lane + i, a.lk - 1);
+            rr[i] = (int)(kb + __ldg(a.perm_k + kb + tok));
+          }
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv) {  // item j = 2u + kv: K_u then V_u
+            const int j = 2 * u + kv, s = j % NSLOT;
+            mbar_wait(&bars.empty[s], ((uint32_t)(j / NSLOT) & 1u) ^ 1u);
+            if (kv == 0 && lane == 0) TR(0, u);
+            if (lane == 0) mbar_expect_tx(&bars.full[s], TILE);
+            __syncwarp();
+            const uint32_t dst = base + SMEM_SLOT + s * TILE + lane * 512;
+            const CUtensorMap *map = kv ? &tm_v : &tm_k;
+            tma_gather4(dst, map, &bars.full[s], 0, rr[0], rr[1], rr[2], rr[3]);
+            tma_gather4(dst + BOX, map, &bars.full[s], 64, rr[0], rr[1], rr[2], rr[3]);
+          }
+        }
+      } else if (lane == 0) {
+        UnionWalk walk;
+        walk.init(mask_a, mask_b);
+        for (int u = 0; u < cnt; ++u) {
+          const int gk = walk.next();
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv) {  // item j = 2u + kv: K_u then V_u
+            const int j = 2 * u + kv, s = j % NSLOT;
+            mbar_wait(&bars.empty[s], ((uint32_t)(j / NSLOT) & 1u) ^ 1u);
+            if (kv == 0) TR(0, u);
+            const uint32_t dst = base + SMEM_SLOT + s * TILE;
+            const CUtensorMap *map = kv ? &tm_v : &tm_k;
+            mbar_expect_tx(&bars.full[s], TILE);
+            tma_load_4d(dst, map, &bars.full[s], 0, gk * BN, (int)hk, (int)b);
+            tma_load_4d(dst + BOX, map, &bars.full[s], 64, gk * BN, (int)hk, (int)b);
+          }
         }
       }
     }
@@ -466,7 +470,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
 
 namespace sm100 {
 namespace pp {
-template <int kMode, int kEmu, bool kStagger = true, bool kGather = false>
+template <int kMode, int kEmu, bool kStagger = true, int kGather = 0>
 cudaError_t launch_mode(const AttnArgs &a, const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, dim3 grid,
                         cudaStream_t st) {
   static bool attr = false;
@@ -491,12 +495,16 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
   using namespace sm100::pp;
   CUtensorMap mq, mk, mv;
   if (!get_encode()) return cudaErrorNotSupported;
-  if (a.gather) {
-    if (!make_gather_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs) || !make_gather_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) ||
-        !make_gather_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs))
-      return cudaErrorInvalidValue;
+  if (a.gather) {  // bit 1: Q through pi_q (gather4); bit 2: K, V through pi_k (gather4)
+    const bool gq = a.gather & 1, gkv = a.gather & 2;
+    const bool ok = (gq ? make_gather_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs) : make_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs, 128)) &&
+                    (gkv ? make_gather_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) && make_gather_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs)
+                         : make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) && make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128));
+    if (!ok) return cudaErrorInvalidValue;
     dim3 grid((unsigned)((a.nq + 1) / 2), (unsigned)(a.batch * a.hq));
-    return launch_mode<0, kDefaultEmu, false, true>(a, mq, mk, mv, grid, st);
+    if (gq && gkv) return launch_mode<0, kDefaultEmu, false, 3>(a, mq, mk, mv, grid, st);
+    if (gkv) return launch_mode<0, kDefaultEmu, false, 2>(a, mq, mk, mv, grid, st);
+    return launch_mode<0, kDefaultEmu, false, 1>(a, mq, mk, mv, grid, st);
   }
   if (!make_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs, 128) || !make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) ||
       !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128))

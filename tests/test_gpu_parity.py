@@ -341,10 +341,14 @@ q, k, v = make_qkv(w, device="cuda", seq_len={L}, heads_q={hq}, heads_kv={hkv}, 
 assert ba.zero_copy_supported(q, k, v, {B})
 c0 = ba.Context(q, k, v, {B}, {dens})
 c1 = ba.Context(q, k, v, {B}, {dens}, zero_copy=True)
-s0 = c0.select(q, k, v); s1 = c1.select(q, k, v)
+c3 = ba.Context(q, k, v, {B}, {dens}, zero_copy="q")
+s0 = c0.select(q, k, v); s1 = c1.select(q, k, v); s3 = c3.select(q, k, v)
 assert s1.q_sorted is None and s1.v_sorted is None
-o0 = torch.empty_like(q); o1 = torch.full_like(q, float("nan"))
-c0.sparse_attn(o0); c1.sparse_attn(o1)
+assert s3.q_sorted is None and s3.k_sorted is not None
+o0 = torch.empty_like(q); o1 = torch.full_like(q, float("nan")); o3 = torch.full_like(q, float("nan"))
+c0.sparse_attn(o0); c1.sparse_attn(o1); c3.sparse_attn(o3)
+assert torch.equal(o0, o3)
+assert torch.equal(s0.k_sorted, s3.k_sorted) and torch.equal(s0.v_sorted, s3.v_sorted)
 o2 = ba.ba_attention(q, k, v, block_size={B}, density={dens})  # copy path
 torch.cuda.synchronize()
 for f in ("perm_q", "perm_k", "kv_index", "kv_count"):
@@ -355,7 +359,7 @@ err = max_abs_err(o1, oracle_output_with_gpu_selection(q, k, v, s1, {B}))
 assert err <= 2e-2, err
 print("OK", ba.attention_kernel_name(q, k, v, {B}))
 """
-    for zc in ("0", "1"):  # ba_attention on the copy path and on BA_ZERO_COPY=1
+    for zc in ("0", "1", "2"):  # ba_attention: copies / BA_ZERO_COPY=1 (none) / =2 (Q in place)
         env = dict(os.environ, BA_ATTN_K5=k5, BA_ZERO_COPY=zc)
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
         assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
