@@ -28,6 +28,7 @@
 //                    TOPP (reading A23): kappa_row from the cumulative mass
 //                    of the (-m', g_k)-ordered row, capped at kappa.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -541,20 +542,135 @@ __global__ void __launch_bounds__(256) scores_kernel(int64_t hq, int64_t grp, in
   }
 }
 
+// The same inner product of length 3d on the FP64 tensor path: mma.sync
+// m8n8k4.f64 (DMMA).  Measured on B200 (tools/dmma_bench.cu) DMMA and DFMA both
+// peak at 128 FLOP/clk/SM, but one DMMA does the work of 8 warp-wide DFMAs per
+// 2 operand loads, so the issue slots and smem reads that held the SIMT kernel
+// to ~39% of peak stop binding.  CTA tile TILE x TILE, warps of 32 x 32 (4 x 4
+// DMMA tiles, 32 fp64 accumulators per thread), kScK = 8 features per stage
+// (2 k-steps of 4), register-staged prefetch of the next stage.
+// Fragments (PTX m8n8k4 .f64): g = lane/4, t = lane%4;  A[g][t], B[t][g],
+// C[g][2t + {0,1}].
+template <int D, int TILE>
+__global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_kernel(
+    int64_t hq, int64_t grp, int64_t nq, int64_t nk, const double *__restrict__ q_mean,
+    const double *__restrict__ q_var, const double *__restrict__ k_mean, const double *__restrict__ k_var,
+    int comp, double inv_sqrt_d, double beta_over_d, double *__restrict__ logits) {
+  constexpr int WARPS = (TILE / 32) * (TILE / 32), NT = WARPS * 32;
+  constexpr int LDS = TILE + 8;                       // k-row stride (doubles): 4 k-rows -> 2 wavefronts
+  constexpr int LPT = TILE * kScK / NT;               // features each thread loads per operand per stage
+  constexpr int TPR = kScK / LPT;                     // loader threads per row
+  __shared__ __align__(16) double As[2][kScK][LDS];
+  __shared__ __align__(16) double Bs[2][kScK][LDS];
+  const int64_t bhq = blockIdx.z;
+  const int64_t b = bhq / hq, h = bhq - b * hq;
+  const int64_t bhk = b * (hq / grp) + h / grp;
+  const int64_t gq0 = (int64_t)blockIdx.y * TILE, gk0 = (int64_t)blockIdx.x * TILE;
+  const double *qm = q_mean + bhq * nq * D, *qv = q_var + bhq * nq * D;
+  const double *km = k_mean + bhk * nk * D, *kv = k_var + bhk * nk * D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = (warp / (TILE / 32)) * 32, wc = (warp % (TILE / 32)) * 32;  // warp tile origin
+  const int g = lane >> 2, tq = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int nfeat = comp ? 3 * D : D;
+  const int lr = threadIdx.x / TPR, lf = (threadIdx.x % TPR) * LPT;
+  const int64_t gq_l = gq0 + lr, gk_l = gk0 + lr;
+  const bool q_ok = gq_l < nq, k_ok = gk_l < nk;
+  double rqm[LPT], rqv[LPT], rkm[LPT], rkv[LPT];
+  auto fetch = [&](int c0) {
+#pragma unroll
+    for (int e2 = 0; e2 < LPT; ++e2) {
+      const int c = c0 + lf + e2;
+      const int part = c / D, tt = c - part * D;
+      rqm[e2] = q_ok ? qm[gq_l * D + tt] : 0.0;
+      rqv[e2] = (q_ok && part == 1) ? qv[gq_l * D + tt] : 0.0;
+      rkm[e2] = (k_ok && part < 2) ? km[gk_l * D + tt] : 0.0;
+      rkv[e2] = (k_ok && part > 0) ? kv[gk_l * D + tt] : 0.0;
+    }
+  };
+  auto stash = [&](int c0, int buf) {  // Xq = [Qbar/sqrt(d), (beta/d) VarQ, (beta/d) Qbar^2], Xk = [Kbar, Kbar^2 + VarK, VarK]
+#pragma unroll
+    for (int e2 = 0; e2 < LPT; ++e2) {
+      const int c = c0 + lf + e2;
+      const int part = c / D;
+      const double m = rqm[e2], k = rkm[e2];
+      As[buf][lf + e2][lr] = part == 0 ? m * inv_sqrt_d : part == 1 ? beta_over_d * rqv[e2] : beta_over_d * (m * m);
+      Bs[buf][lf + e2][lr] = part == 0 ? k : part == 1 ? fma(k, k, rkv[e2]) : rkv[e2];
+    }
+  };
+  fetch(0);
+  stash(0, 0);
+  __syncthreads();
+  int buf = 0;
+  for (int c0 = 0; c0 < nfeat; c0 += kScK) {
+    const bool more = c0 + kScK < nfeat;
+    if (more) fetch(c0 + kScK);
+#pragma unroll
+    for (int k4 = 0; k4 < kScK; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        af[i] = As[buf][k4 + tq][wr + 8 * i + g];
+        bf[i] = Bs[buf][k4 + tq][wc + 8 * i + g];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                       : "d"(af[i]), "d"(bf[j]));
+    }
+    if (more) stash(c0 + kScK, buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gq = gq0 + wr + 8 * i + g;
+    if (gq >= nq) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gk = gk0 + wc + 8 * j + 2 * tq;
+      double *dst = logits + (bhq * nq + gq) * nk + gk;
+      if (gk + 1 < nk && ((nk & 1) == 0)) {
+        *reinterpret_cast<double2 *>(dst) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        if (gk < nk) dst[0] = acc[i][j][0];
+        if (gk + 1 < nk) dst[1] = acc[i][j][1];
+      }
+    }
+  }
+}
+
 cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk,
                           const double *q_mean, const double *q_var, const double *k_mean,
                           const double *k_var, int comp, double beta, double *logits,
                           cudaStream_t st) {
   const double inv_sqrt_d = 1.0 / sqrt((double)d), bod = beta / (double)d;
   const int64_t grp = hq / hkv;
-  // 128-tiles (4x fewer smem reads per FMA) unless that leaves under ~4 CTAs per SM
+  // 128-tiles (16 warps) unless that leaves under ~2 CTAs per SM; BA_SCORES_SIMT=1 selects
+  // the SIMT DFMA kernel (A/B profiling knob)
   const int64_t big = ((nk + 127) / 128) * ((nq + 127) / 128) * batch * hq;
   const int tile = big >= 2 * 148 ? 128 : 64;
+  static int simt = -1;
+  if (simt < 0) simt = getenv("BA_SCORES_SIMT") ? atoi(getenv("BA_SCORES_SIMT")) : 0;
   dim3 grid((unsigned)((nk + tile - 1) / tile), (unsigned)((nq + tile - 1) / tile), (unsigned)(batch * hq));
+  if (simt) {
 #define BA_SC(D, T) scores_kernel<D, T><<<grid, 256, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits)
-  if (d == 128) { if (tile == 128) BA_SC(128, 128); else BA_SC(128, 64); }
-  else { if (tile == 128) BA_SC(64, 128); else BA_SC(64, 64); }
+    if (d == 128) { if (tile == 128) BA_SC(128, 128); else BA_SC(128, 64); }
+    else { if (tile == 128) BA_SC(64, 128); else BA_SC(64, 64); }
 #undef BA_SC
+    return cudaGetLastError();
+  }
+#define BA_SM(D, T) scores_mma_kernel<D, T><<<grid, (T / 32) * (T / 32) * 32, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits)
+  if (d == 128) { if (tile == 128) BA_SM(128, 128); else BA_SM(128, 64); }
+  else { if (tile == 128) BA_SM(64, 128); else BA_SM(64, 64); }
+#undef BA_SM
   return cudaGetLastError();
 }
 
