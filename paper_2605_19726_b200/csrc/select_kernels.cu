@@ -170,8 +170,15 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(SortGeom g, co
   __syncthreads();
   const TileLoc loc = locate_tile(g, t);
   const uint32_t *src = keys + loc.seg_start + loc.tile_off;
-  for (int64_t i = threadIdx.x; i < loc.count; i += kSortThreads)
-    atomicAdd(&h[(__ldg(src + i) >> shift) & 255u], 1u);
+  uint32_t kv[kSortIPT];  // all loads in flight first
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r) {
+    const int64_t i = threadIdx.x + (int64_t)r * kSortThreads;
+    kv[r] = i < loc.count ? __ldg(src + i) : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r)
+    if (threadIdx.x + (int64_t)r * kSortThreads < loc.count) atomicAdd(&h[(kv[r] >> shift) & 255u], 1u);
   __syncthreads();
   hist[t * 256 + threadIdx.x] = h[threadIdx.x];
 }
@@ -233,13 +240,20 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   const int64_t base = loc.seg_start + loc.tile_off;
   uint32_t key[kSortIPT], val[kSortIPT], rank[kSortIPT];
   const unsigned lt = lanemask_lt();
+  // every global load in flight before the ranking rounds (their smem atomics and
+  // __syncwarp would otherwise serialise one load latency per round)
 #pragma unroll
   for (int r = 0; r < kSortIPT; ++r) {
     const int item = warp * kPerWarp + r * 32 + lane;
     const bool valid = item < loc.count;
-    key[r] = valid ? keys_in[base + item] : 0xffffffffu;
+    key[r] = valid ? __ldg(keys_in + base + item) : 0xffffffffu;
     if constexpr (kFirst) val[r] = (uint32_t)(loc.win_start + loc.tile_off + item);
-    else val[r] = valid ? vals_in[base + item] : 0u;
+    else val[r] = valid ? __ldg(vals_in + base + item) : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r) {
+    const int item = warp * kPerWarp + r * 32 + lane;
+    const bool valid = item < loc.count;
     const uint32_t digit = (key[r] >> shift) & 255u;
     const unsigned vmask = __ballot_sync(0xffffffffu, valid);
     rank[r] = 0;
@@ -346,7 +360,10 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
   constexpr int CPR = D / EPC;       // chunks per row
   constexpr int RPI = 256 / CPR;     // rows per iteration
   constexpr int MAXIT = 128 / RPI;   // B <= 128
-  __shared__ double red[2][RPI][D + 1];
+  static_assert(CPR * 2 == 32 || CPR == 32 || CPR * 4 == 32, "row groups per warp");
+  constexpr int GPW = 32 / CPR;                 // row groups per warp (combined by shuffles)
+  constexpr int RG = RPI / GPW;                 // partial rows left for the smem reduction
+  __shared__ double red[2][RG][D + 1];
   __shared__ double s_shift[D];
   const int64_t g = blockIdx.x;
   const int64_t bh = blockIdx.y;  // batch * heads + head
@@ -409,7 +426,17 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
     }
   }
 #pragma unroll
-  for (int e = 0; e < EPC; ++e) { red[0][rsub][chunk * EPC + e] = a1[e]; red[1][rsub][chunk * EPC + e] = a2[e]; }
+  for (int e = 0; e < EPC; ++e) {
+#pragma unroll
+    for (int off = CPR; off < 32; off <<= 1) {
+      a1[e] += __shfl_xor_sync(0xffffffffu, a1[e], off);
+      a2[e] += __shfl_xor_sync(0xffffffffu, a2[e], off);
+    }
+  }
+  if ((threadIdx.x & 31) < CPR) {
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) { red[0][rsub / GPW][chunk * EPC + e] = a1[e]; red[1][rsub / GPW][chunk * EPC + e] = a2[e]; }
+  }
   if (rsub == 0) {
 #pragma unroll
     for (int e = 0; e < EPC; ++e) s_shift[chunk * EPC + e] = kc[e];
@@ -419,7 +446,8 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
   const int64_t nb = (L + B - 1) / B;
   for (int c = threadIdx.x; c < D; c += 256) {
     double t1 = 0.0, t2 = 0.0;
-    for (int i = 0; i < RPI; ++i) { t1 += red[0][i][c]; t2 += red[1][i][c]; }
+#pragma unroll
+    for (int i = 0; i < RG; ++i) { t1 += red[0][i][c]; t2 += red[1][i][c]; }
     const double m1 = t1 * inv_n;
     mean[(bh * nb + g) * D + c] = s_shift[c] + m1;
     var[(bh * nb + g) * D + c] = fmax(fma(-m1, m1, t2 * inv_n), 0.0);
