@@ -570,26 +570,28 @@ __global__ void __launch_bounds__(256) scores_kernel(int64_t hq, int64_t grp, in
   }
 }
 
+constexpr int kScoresKS = 8;   // features per smem stage of the DMMA kernel (32: register and smem budget exceeded)
+
 // The same inner product of length 3d on the FP64 tensor path: mma.sync
 // m8n8k4.f64 (DMMA).  Measured on B200 (tools/dmma_bench.cu) DMMA and DFMA both
 // peak at 128 FLOP/clk/SM, but one DMMA does the work of 8 warp-wide DFMAs per
 // 2 operand loads, so the issue slots and smem reads that held the SIMT kernel
 // to ~39% of peak stop binding.  CTA tile TILE x TILE, warps of 32 x 32 (4 x 4
-// DMMA tiles, 32 fp64 accumulators per thread), kScK = 8 features per stage
-// (2 k-steps of 4), register-staged prefetch of the next stage.
+// DMMA tiles, 32 fp64 accumulators per thread), KS features per stage (KS/4
+// k-steps of 4), register-staged prefetch of the next stage.
 // Fragments (PTX m8n8k4 .f64): g = lane/4, t = lane%4;  A[g][t], B[t][g],
 // C[g][2t + {0,1}].
-template <int D, int TILE>
+template <int D, int TILE, int KS>
 __global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_kernel(
     int64_t hq, int64_t grp, int64_t nq, int64_t nk, const double *__restrict__ q_mean,
     const double *__restrict__ q_var, const double *__restrict__ k_mean, const double *__restrict__ k_var,
     int comp, double inv_sqrt_d, double beta_over_d, double *__restrict__ logits) {
   constexpr int WARPS = (TILE / 32) * (TILE / 32), NT = WARPS * 32;
   constexpr int LDS = TILE + 8;                       // k-row stride (doubles): 4 k-rows -> 2 wavefronts
-  constexpr int LPT = TILE * kScK / NT;               // features each thread loads per operand per stage
-  constexpr int TPR = kScK / LPT;                     // loader threads per row
-  __shared__ __align__(16) double As[2][kScK][LDS];
-  __shared__ __align__(16) double Bs[2][kScK][LDS];
+  constexpr int LPT = TILE * KS / NT;               // features each thread loads per operand per stage
+  constexpr int TPR = KS / LPT;                     // loader threads per row
+  __shared__ __align__(16) double As[2][KS][LDS];
+  __shared__ __align__(16) double Bs[2][KS][LDS];
   const int64_t bhq = blockIdx.z;
   const int64_t b = bhq / hq, h = bhq - b * hq;
   const int64_t bhk = b * (hq / grp) + h / grp;
@@ -634,11 +636,11 @@ __global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_ker
   stash(0, 0);
   __syncthreads();
   int buf = 0;
-  for (int c0 = 0; c0 < nfeat; c0 += kScK) {
-    const bool more = c0 + kScK < nfeat;
-    if (more) fetch(c0 + kScK);
+  for (int c0 = 0; c0 < nfeat; c0 += KS) {
+    const bool more = c0 + KS < nfeat;
+    if (more) fetch(c0 + KS);
 #pragma unroll
-    for (int k4 = 0; k4 < kScK; k4 += 4) {
+    for (int k4 = 0; k4 < KS; k4 += 4) {
       double af[4], bf[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -653,7 +655,7 @@ __global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_ker
                        : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
                        : "d"(af[i]), "d"(bf[j]));
     }
-    if (more) stash(c0 + kScK, buf ^ 1);
+    if (more) stash(c0 + KS, buf ^ 1);
     __syncthreads();
     buf ^= 1;
   }
@@ -695,7 +697,7 @@ cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t
 #undef BA_SC
     return cudaGetLastError();
   }
-#define BA_SM(D, T) scores_mma_kernel<D, T><<<grid, (T / 32) * (T / 32) * 32, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits)
+#define BA_SM(D, T) scores_mma_kernel<D, T, kScoresKS><<<grid, (T / 32) * (T / 32) * 32, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits)
   if (d == 128) { if (tile == 128) BA_SM(128, 128); else BA_SM(128, 64); }
   else { if (tile == 128) BA_SM(64, 128); else BA_SM(64, 64); }
 #undef BA_SM
