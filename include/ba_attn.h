@@ -77,10 +77,13 @@ typedef enum { BA_DTYPE_BF16 = 0, BA_DTYPE_FP32 = 1 } ba_dtype;
 /* Which sides are norm-ranked (ablation Table). */
 typedef enum { BA_SORT_NONE = 0, BA_SORT_Q = 1, BA_SORT_K = 2, BA_SORT_QK = 3 } ba_sort_mode;
 
-/* Compensation of the block logits: none, or the diagonal-variance form
+/* Compensation of the block logits: none; the diagonal-variance form
  * Delta = (1/d) sum_t (VarQ_t Kbar_t^2 + VarK_t Qbar_t^2 + VarQ_t VarK_t)
- * (Eq. diag-variance-form). */
-typedef enum { BA_COMP_NONE = 0, BA_COMP_DIAG = 1 } ba_comp_mode;
+ * (Eq. diag-variance-form), the default; or the exact covariance
+ * form Delta = (1/d) tr(SigmaQ SigmaK) with full per-block covariances
+ * (Eq. cov-comp; NEXT-4) — O(N d^2) workspace per side and
+ * 2 N_q N_k d^2 FLOP per head, for small L and diagnostics. */
+typedef enum { BA_COMP_NONE = 0, BA_COMP_DIAG = 1, BA_COMP_EXACT = 2 } ba_comp_mode;
 
 /* Budget rule ("under different computational budgets"; Alg. 1 step 10
  * P:560 top-kappa).

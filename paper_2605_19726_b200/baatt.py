@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("BA_LIB_PATH") or os.path.join(HERE, "libbaatt.so")  #
 
 BA_DTYPE_BF16, BA_DTYPE_FP32 = 0, 1
 SORT = {"none": 0, "q": 1, "k": 2, "qk": 3}
-COMP = {"none": 0, "diag": 1}
+COMP = {"none": 0, "diag": 1, "exact": 2}
 SELECT_TOPK, SELECT_TOPP = 0, 1
 
 

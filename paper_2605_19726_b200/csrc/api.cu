@@ -65,7 +65,8 @@ ba_status check_problem(const ba_problem *p, const ba_params *pa, Dims *o) {
   if (p->block_size != 64 && p->block_size != 128) return fail(BA_ERR_UNSUPPORTED, "block_size = %d (supported: 64, 128)", p->block_size);
   if (p->dtype != BA_DTYPE_BF16 && p->dtype != BA_DTYPE_FP32) return fail(BA_ERR_INVALID_ARGUMENT, "dtype = %d", p->dtype);
   if (pa->sort < BA_SORT_NONE || pa->sort > BA_SORT_QK) return fail(BA_ERR_INVALID_ARGUMENT, "sort = %d", pa->sort);
-  if (pa->comp != BA_COMP_NONE && pa->comp != BA_COMP_DIAG) return fail(BA_ERR_INVALID_ARGUMENT, "comp = %d", pa->comp);
+  if (pa->comp != BA_COMP_NONE && pa->comp != BA_COMP_DIAG && pa->comp != BA_COMP_EXACT)
+    return fail(BA_ERR_INVALID_ARGUMENT, "comp = %d", pa->comp);
   if (pa->select != BA_SELECT_TOPK && pa->select != BA_SELECT_TOPP) return fail(BA_ERR_INVALID_ARGUMENT, "select = %d", pa->select);
   if (pa->select == BA_SELECT_TOPP && !(pa->top_p > 0.f && pa->top_p <= 1.f))
     return fail(BA_ERR_INVALID_ARGUMENT, "top_p = %g not in (0, 1]", (double)pa->top_p);
@@ -132,7 +133,7 @@ SortGeom make_geom(const Dims &D, const ba_params *pa) {
 }
 
 struct SelectPlan {
-  size_t keys_a, vals_a, keys_b, vals_b, hist, q_mean, q_var, k_mean, k_var, logits, total;
+  size_t keys_a, vals_a, keys_b, vals_b, hist, q_mean, q_var, k_mean, k_var, q_cov, k_cov, logits, total;
 };
 
 SelectPlan plan_select(const Dims &D, const ba_params *pa, const ba_selection *sel) {
@@ -151,6 +152,10 @@ SelectPlan plan_select(const Dims &D, const ba_params *pa, const ba_selection *s
   p.k_mean = (sel && sel->k_mean) ? SIZE_MAX : take(ks);
   p.k_var = (sel && sel->k_var) ? SIZE_MAX : take(ks);
   p.logits = (sel && sel->logits) ? SIZE_MAX : take(8ull * D.b * D.hq * D.nq * D.nk);
+  if (pa->comp == BA_COMP_EXACT) {  // NEXT-4: block covariances [b, H, N, d, d] fp64
+    p.q_cov = take(8ull * D.b * D.hq * D.nq * D.d * D.d);
+    p.k_cov = take(8ull * D.b * D.hkv * D.nk * D.d * D.d);
+  }
   p.total = off;
   return p;
 }
@@ -251,8 +256,19 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   }
   // K4: scores, then per-row top-kappa
   double *logits = sel->logits ? sel->logits : at<double>(ws, plan.logits);
-  BA_TRY(cuda_check(launch_scores((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, q_var, k_mean, k_var,
-                                  pa->comp == BA_COMP_DIAG ? 1 : 0, (double)pa->beta, logits, st), "scores"));
+  if (pa->comp == BA_COMP_EXACT) {  // NEXT-4: Delta = tr(SigmaQ SigmaK)/d (Eq. cov-comp)
+    double *q_cov = at<double>(ws, plan.q_cov), *k_cov = at<double>(ws, plan.k_cov);
+    BA_TRY(cuda_check(launch_block_cov(D.dtype, (int)D.d, q, prob->q_stride, D.b, D.hq, D.lq, (int)D.B,
+                                       sort_q(pa) ? sel->perm_q : nullptr, q_mean, q_cov, st), "block_cov(q)"));
+    BA_TRY(cuda_check(launch_block_cov(D.dtype, (int)D.d, k, prob->k_stride, D.b, D.hkv, D.lk, (int)D.B,
+                                       sort_k(pa) ? sel->perm_k : nullptr, k_mean, k_cov, st), "block_cov(k)"));
+    launches += 2;
+    BA_TRY(cuda_check(launch_scores((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, q_cov, k_mean, k_cov, 2,
+                                    (double)pa->beta, logits, st), "scores"));
+  } else {
+    BA_TRY(cuda_check(launch_scores((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, q_var, k_mean, k_var,
+                                    pa->comp == BA_COMP_DIAG ? 1 : 0, (double)pa->beta, logits, st), "scores"));
+  }
   const double top_p = pa->select == BA_SELECT_TOPP ? (double)pa->top_p : 0.0;
   BA_TRY(cuda_check(launch_topk(D.b * D.hq * D.nq, D.nk, D.kappa, top_p, logits, sel->kv_index, sel->kv_count,
                                 sel->mask, sel->block_prob, sel->threshold, st), "topk"));

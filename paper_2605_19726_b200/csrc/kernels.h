@@ -46,6 +46,10 @@ cudaError_t launch_gather_stats(int dtype, int d, const void *x, const int64_t *
                                 int64_t heads, int64_t L, int B, const int32_t *perm,
                                 int32_t *perm_identity_out, void *xs, double *mean, double *var,
                                 cudaStream_t st);
+// NEXT-4: per-block covariance [b, H, N, d, d] fp64 of the rows x[pi] (perm NULL = identity)
+cudaError_t launch_block_cov(int dtype, int d, const void *x, const int64_t *stride, int64_t batch, int64_t heads,
+                             int64_t L, int B, const int32_t *perm, const double *mean, double *cov, cudaStream_t st);
+// comp: 0 none, 1 diagonal (q_var / k_var = variances), 2 exact (q_var / k_var = covariances)
 cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk,
                           const double *q_mean, const double *q_var, const double *k_mean,
                           const double *k_var, int comp, double beta, double *logits,

@@ -469,6 +469,82 @@ cudaError_t launch_gather_stats(int dtype, int d, const void *x, const int64_t *
 }
 
 // =====================================================================================
+// K3b (NEXT-4): per-block covariance Sigma_g = (1/n) sum_i (x_i - xbar)(x_i - xbar)^T
+// in fp64 for the exact compensation tr(SigmaQ SigmaK)/d (Eq. cov-comp,
+// P:494-495).  One CTA (256 threads) per (block, batch*head); rows are read through
+// pi (like K3) 16 at a time, centred in fp64 into smem, and each thread accumulates
+// a (D/16) x (D/16) patch: rows ty + 16 i, columns tx + 16 j (conflict-free reads).
+// =====================================================================================
+template <typename T, int D>
+__global__ void __launch_bounds__(256) block_cov_kernel(const T *__restrict__ x, int64_t s0, int64_t s1, int64_t s2,
+                                                        int64_t heads, int64_t L, int B, const int32_t *__restrict__ perm,
+                                                        const double *__restrict__ mean, double *__restrict__ cov) {
+  constexpr int R = D / 16;
+  constexpr int EPC = Chunk<T>::EPC, CPR = D / EPC, RPC = 256 / CPR;  // rows per load pass
+  constexpr int CH = 16;                                               // rows per smem chunk
+  __shared__ double xc[CH][D + 1];
+  __shared__ double mu[D];
+  const int64_t g = blockIdx.x, bh = blockIdx.y;
+  const int64_t b = bh / heads, h = bh - b * heads;
+  const int64_t nb = (L + B - 1) / B;
+  const int64_t row0 = g * B;
+  const int n = (int)imin64(B, L - row0);
+  for (int c = threadIdx.x; c < D; c += 256) mu[c] = mean[(bh * nb + g) * D + c];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[R][R];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < R; ++j) acc[i][j] = 0.0;
+  const T *xbase = x + b * s0 + h * s1;
+  const int chunk = threadIdx.x % CPR, rsub = threadIdx.x / CPR;
+  __syncthreads();
+  for (int r0 = 0; r0 < n; r0 += CH) {
+    for (int rr = rsub; rr < CH; rr += RPC) {
+      const int r = r0 + rr;
+      float v[EPC];
+      if (r < n) {
+        const int64_t tok = row0 + r;
+        const int64_t src = perm ? (int64_t)__ldg(perm + bh * L + tok) : tok;
+        Chunk<T>::unpack(ldg16(xbase + src * s2 + chunk * EPC), v);
+      }
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) xc[rr][chunk * EPC + e] = r < n ? (double)v[e] - mu[chunk * EPC + e] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < CH; ++rr) {
+      double a[R], c2[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) { a[i] = xc[rr][ty + 16 * i]; c2[i] = xc[rr][tx + 16 * i]; }
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = 0; j < R; ++j) acc[i][j] = fma(a[i], c2[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const double inv_n = 1.0 / (double)n;
+  double *out = cov + (bh * nb + g) * (int64_t)D * D;
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < R; ++j) out[(ty + 16 * i) * D + tx + 16 * j] = acc[i][j] * inv_n;
+}
+
+cudaError_t launch_block_cov(int dtype, int d, const void *x, const int64_t *st, int64_t batch, int64_t heads, int64_t L,
+                             int B, const int32_t *perm, const double *mean, double *cov, cudaStream_t stream) {
+  dim3 grid((unsigned)((L + B - 1) / B), (unsigned)(batch * heads));
+#define BA_BC(T, D) block_cov_kernel<T, D><<<grid, 256, 0, stream>>>((const T *)x, st[0], st[1], st[2], heads, L, B, perm, mean, cov)
+  if (dtype == 0 && d == 128) BA_BC(__nv_bfloat16, 128);
+  else if (dtype == 0 && d == 64) BA_BC(__nv_bfloat16, 64);
+  else if (dtype == 1 && d == 128) BA_BC(float, 128);
+  else BA_BC(float, 64);
+#undef BA_BC
+  return cudaGetLastError();
+}
+
+// =====================================================================================
 // K4a: compensated block logits as an fp64 micro-GEMM over 3d features.
 // =====================================================================================
 constexpr int kScK = 8;  // features per smem stage
@@ -581,7 +657,11 @@ constexpr int kScoresKS = 8;   // features per smem stage of the DMMA kernel (32
 // k-steps of 4), register-staged prefetch of the next stage.
 // Fragments (PTX m8n8k4 .f64): g = lane/4, t = lane%4;  A[g][t], B[t][g],
 // C[g][2t + {0,1}].
-template <int D, int TILE, int KS>
+// kExact (NEXT-4, Eq. cov-comp): l' = Qbar.Kbar/sqrt(d) + (beta/d) tr(SigmaQ SigmaK)
+// = one inner product of length d + d^2 with Xq = [Qbar/sqrt(d), (beta/d) vec SigmaQ] and
+// Xk = [Kbar, vec SigmaK] (the covariances are symmetric: tr(AB) = vec(A).vec(B));
+// q_var / k_var then point at the covariances [.., N, d, d].
+template <int D, int TILE, int KS, bool kExact = false>
 __global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_kernel(
     int64_t hq, int64_t grp, int64_t nq, int64_t nk, const double *__restrict__ q_mean,
     const double *__restrict__ q_var, const double *__restrict__ k_mean, const double *__restrict__ k_var,
@@ -596,8 +676,9 @@ __global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_ker
   const int64_t b = bhq / hq, h = bhq - b * hq;
   const int64_t bhk = b * (hq / grp) + h / grp;
   const int64_t gq0 = (int64_t)blockIdx.y * TILE, gk0 = (int64_t)blockIdx.x * TILE;
-  const double *qm = q_mean + bhq * nq * D, *qv = q_var + bhq * nq * D;
-  const double *km = k_mean + bhk * nk * D, *kv = k_var + bhk * nk * D;
+  constexpr int64_t VW = kExact ? D * D : D;  // per-block width of q_var / k_var
+  const double *qm = q_mean + bhq * nq * D, *qv = q_var + bhq * nq * VW;
+  const double *km = k_mean + bhk * nk * D, *kv = k_var + bhk * nk * VW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wr = (warp / (TILE / 32)) * 32, wc = (warp % (TILE / 32)) * 32;  // warp tile origin
   const int g = lane >> 2, tq = lane & 3;
@@ -606,7 +687,7 @@ __global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_ker
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const int nfeat = comp ? 3 * D : D;
+  const int nfeat = kExact ? D + D * D : comp ? 3 * D : D;
   const int lr = threadIdx.x / TPR, lf = (threadIdx.x % TPR) * LPT;
   const int64_t gq_l = gq0 + lr, gk_l = gk0 + lr;
   const bool q_ok = gq_l < nq, k_ok = gk_l < nk;
@@ -615,21 +696,31 @@ __global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_ker
 #pragma unroll
     for (int e2 = 0; e2 < LPT; ++e2) {
       const int c = c0 + lf + e2;
-      const int part = c / D, tt = c - part * D;
-      rqm[e2] = q_ok ? qm[gq_l * D + tt] : 0.0;
-      rqv[e2] = (q_ok && part == 1) ? qv[gq_l * D + tt] : 0.0;
-      rkm[e2] = (k_ok && part < 2) ? km[gk_l * D + tt] : 0.0;
-      rkv[e2] = (k_ok && part > 0) ? kv[gk_l * D + tt] : 0.0;
+      if constexpr (kExact) {  // c < D: the means; c >= D: vec(Sigma) entry c - D
+        rqm[e2] = q_ok ? (c < D ? qm[gq_l * D + c] : qv[gq_l * VW + (c - D)]) : 0.0;
+        rkm[e2] = k_ok ? (c < D ? km[gk_l * D + c] : kv[gk_l * VW + (c - D)]) : 0.0;
+      } else {
+        const int part = c / D, tt = c - part * D;
+        rqm[e2] = q_ok ? qm[gq_l * D + tt] : 0.0;
+        rqv[e2] = (q_ok && part == 1) ? qv[gq_l * D + tt] : 0.0;
+        rkm[e2] = (k_ok && part < 2) ? km[gk_l * D + tt] : 0.0;
+        rkv[e2] = (k_ok && part > 0) ? kv[gk_l * D + tt] : 0.0;
+      }
     }
   };
   auto stash = [&](int c0, int buf) {  // Xq = [Qbar/sqrt(d), (beta/d) VarQ, (beta/d) Qbar^2], Xk = [Kbar, Kbar^2 + VarK, VarK]
 #pragma unroll
     for (int e2 = 0; e2 < LPT; ++e2) {
       const int c = c0 + lf + e2;
-      const int part = c / D;
-      const double m = rqm[e2], k = rkm[e2];
-      As[buf][lf + e2][lr] = part == 0 ? m * inv_sqrt_d : part == 1 ? beta_over_d * rqv[e2] : beta_over_d * (m * m);
-      Bs[buf][lf + e2][lr] = part == 0 ? k : part == 1 ? fma(k, k, rkv[e2]) : rkv[e2];
+      if constexpr (kExact) {
+        As[buf][lf + e2][lr] = c < D ? rqm[e2] * inv_sqrt_d : beta_over_d * rqm[e2];
+        Bs[buf][lf + e2][lr] = rkm[e2];
+      } else {
+        const int part = c / D;
+        const double m = rqm[e2], k = rkm[e2];
+        As[buf][lf + e2][lr] = part == 0 ? m * inv_sqrt_d : part == 1 ? beta_over_d * rqv[e2] : beta_over_d * (m * m);
+        Bs[buf][lf + e2][lr] = part == 0 ? k : part == 1 ? fma(k, k, rkv[e2]) : rkv[e2];
+      }
     }
   };
   fetch(0);
@@ -690,16 +781,21 @@ cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t
   static int simt = -1;
   if (simt < 0) simt = getenv("BA_SCORES_SIMT") ? atoi(getenv("BA_SCORES_SIMT")) : 0;
   dim3 grid((unsigned)((nk + tile - 1) / tile), (unsigned)((nq + tile - 1) / tile), (unsigned)(batch * hq));
-  if (simt) {
+  if (simt && comp != 2) {
 #define BA_SC(D, T) scores_kernel<D, T><<<grid, 256, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits)
     if (d == 128) { if (tile == 128) BA_SC(128, 128); else BA_SC(128, 64); }
     else { if (tile == 128) BA_SC(64, 128); else BA_SC(64, 64); }
 #undef BA_SC
     return cudaGetLastError();
   }
-#define BA_SM(D, T) scores_mma_kernel<D, T, kScoresKS><<<grid, (T / 32) * (T / 32) * 32, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits)
-  if (d == 128) { if (tile == 128) BA_SM(128, 128); else BA_SM(128, 64); }
-  else { if (tile == 128) BA_SM(64, 128); else BA_SM(64, 64); }
+#define BA_SM(D, T, X) scores_mma_kernel<D, T, kScoresKS, X><<<grid, (T / 32) * (T / 32) * 32, 0, st>>>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, bod, logits)
+  if (comp == 2) {  // exact covariance compensation: q_var / k_var are the block covariances
+    if (d == 128) { if (tile == 128) BA_SM(128, 128, true); else BA_SM(128, 64, true); }
+    else { if (tile == 128) BA_SM(64, 128, true); else BA_SM(64, 64, true); }
+    return cudaGetLastError();
+  }
+  if (d == 128) { if (tile == 128) BA_SM(128, 128, false); else BA_SM(128, 64, false); }
+  else { if (tile == 128) BA_SM(64, 128, false); else BA_SM(64, 64, false); }
 #undef BA_SM
   return cudaGetLastError();
 }

@@ -19,7 +19,7 @@ import oracle as O
 MASK_BAND = 1e-6
 TOL = {torch.bfloat16: 2e-2, torch.float32: 1e-5}
 SORT_CODE = {"none": O.SORT_NONE, "q": O.SORT_Q, "k": O.SORT_K, "qk": O.SORT_QK}
-COMP_CODE = {"none": O.COMP_NONE, "diag": O.COMP_DIAG}
+COMP_CODE = {"none": O.COMP_NONE, "diag": O.COMP_DIAG, "exact": O.COMP_EXACT}
 
 
 def oracle_select_all(q, k, B, density, beta, sort, comp, window=None, heads=None, top_p=None):

@@ -104,6 +104,7 @@ def test_sizes_and_kappa(ba):
     (lambda p, pa: setattr(pa, "select", 1), "INVALID_ARGUMENT"),          # TOPP with top_p = 0
     (lambda p, pa: (setattr(pa, "select", 1), setattr(pa, "top_p", 1.01)), "INVALID_ARGUMENT"),
     (lambda p, pa: setattr(pa, "select", 2), "INVALID_ARGUMENT"),
+    (lambda p, pa: setattr(pa, "comp", 3), "INVALID_ARGUMENT"),
 ])
 def test_validation_errors(ba, mutate, code):
     q, k, v = _meta(1, 4, 2, 1000, 128)
@@ -159,3 +160,15 @@ def test_kernel_routing(ba):
     assert ba.attention_kernel_name(q, k, v, 64) == "attn_sm100_tcgen05_dual64"
     q, k, v = _meta(1, 1, 1, 1024, 64, torch.float32)
     assert ba.attention_kernel_name(q, k, v, 64) == "attn_simt"
+
+
+def test_exact_compensation_workspace(ba):
+    """BA_COMP_EXACT (NEXT-4) carves the per-block covariances [b, H, N, d, d]
+    fp64 of both sides from the select workspace."""
+    lib = ba.load()
+    q, k, v = _meta(1, 4, 2, 2048, 128)
+    p = ba.make_problem(q, k, v)
+    diag = lib.ba_select_workspace_size(ctypes.byref(p), ctypes.byref(ba.make_params(comp="diag")))
+    exact = lib.ba_select_workspace_size(ctypes.byref(p), ctypes.byref(ba.make_params(comp="exact")))
+    n = 2048 // 128
+    assert exact - diag >= 8 * 128 * 128 * n * (4 + 2)

@@ -380,3 +380,30 @@ def test_zero_copy_unsupported_layout_falls_back_to_copies(ba):
     ref = ba.ba_attention(q, k, v)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+# ---------------------------------------------------------------- NEXT-4: exact covariance compensation
+@pytest.mark.parametrize("cfg,L,hq,hkv,B,dens,beta", [
+    ("T", 1024, 1, 1, 64, 0.5, 1.0),          # fp32, d = 64
+    ("A", 2048 + 77, 2, 2, 128, 0.5, 1.0),    # ragged last block
+    ("C", 1024 * 3, 4, 1, 128, 0.25, 0.5),    # GQA, beta != 1
+    ("M", 1024 + 13, 2, 2, 64, 0.5, 1.0),
+])
+def test_selection_exact_compensation(ba, cfg, L, hq, hkv, B, dens, beta):
+    """BA_COMP_EXACT: Delta = tr(SigmaQ SigmaK)/d from full per-block covariances
+    (Eq. cov-comp) — masks within the band of the oracle's
+    compensation_exact selection, m' within 1e-12, outputs within tolerance."""
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv)
+    ctx = ba.Context(q, k, v, B, dens, beta, "qk", "exact", diagnostics=True)
+    sel = ctx.select(q, k, v)
+    out = torch.empty_like(q)
+    ctx.sparse_attn(out)
+    torch.cuda.synchronize()
+    ref = oracle_select_all(q, k, B, dens, beta, "qk", "exact")
+    rep = check_selection(sel, ref)
+    assert rep["max_abs_dm"] < 1e-12, rep
+    # and the exact rule differs from the diagonal one somewhere (the test is not vacuous)
+    diag = oracle_select_all(q, k, B, dens, beta, "qk", "diag")
+    assert any(np.abs(ref[kk].m - diag[kk].m).max() > 1e-9 for kk in ref)
+    assert max_abs_err(out, oracle_output_with_gpu_selection(q, k, v, sel, B)) <= TOL[q.dtype]
