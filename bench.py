@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--q-in-place", action="store_true", help="no Q' copy: Q read through pi_q (K'/V' copies)")
+    ap.add_argument("--comp", default="diag", choices=["none", "diag", "exact"],
+                    help="compensation: diagonal (default), none, or exact covariances (NEXT-4)")
+    ap.add_argument("--fidelity", action="store_true",
+                    help="NEXT-3: also report the oracle block mass (ba_block_mass): captured mass, Pearson R(m', m_hat)")
     ap.add_argument("--zero-copy", action="store_true",
                     help="NEXT-2: no Q'/K'/V' copies, attention gathers rows through pi (ba_sparse_attn_gather)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -67,11 +71,11 @@ def load_peaks():
     return {"tflops_burst": 1590.0, "tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "source": "fallback"}
 
 
-def workload_desc(w, density, top_p=None):
+def workload_desc(w, density, top_p=None, comp="diag"):
     budget = (f"density={density} ({int(round((1 - density) * 100))}% block sparsity)" if top_p is None else
               f"top_p={top_p} capped at density={density} (cumulative-mass budget)")
     return (f"{w.name} (config {w.config_index}): per rank b=1, Hq={w.heads_q}, Hkv={w.heads_kv}, "
-            f"L={w.seq_len}, d={w.head_dim}, B={w.block_size}, {budget}, sort=qk, comp=diag, beta=1")
+            f"L={w.seq_len}, d={w.head_dim}, B={w.block_size}, {budget}, sort=qk, comp={comp}, beta=1")
 
 
 # --------------------------------------------------------------------------- clocks
@@ -247,7 +251,7 @@ def run_ours(args):
     # (no copies), --q-in-place only Q read through pi_q
     zero_copy = (True if args.zero_copy and ba.zero_copy_supported(q, k, v, w.block_size)
                  else "q" if args.q_in_place and ba.q_gather_supported(q, k, v, w.block_size) else False)
-    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag", top_p=args.top_p, zero_copy=zero_copy)
+    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", args.comp, top_p=args.top_p, zero_copy=zero_copy)
     out = torch.empty_like(q)
     stream = torch.cuda.current_stream()
 
@@ -361,6 +365,30 @@ def run_ours(args):
                "api": "ba_attention_host (pinned host q/k/v -> H2D -> select + sparse attn -> D2H out)"}
         del ws, qh, kh, vh, oh
 
+    fidelity = None
+    if args.fidelity and w.block_size == 128 and not args.profile:
+        # NEXT-3 diagnostics on the GPU: m_hat (Eq. oracle-dist) of the dense softmax in the sorted
+        # block space vs the selection's m': captured mass and Pearson R per head
+        fctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", args.comp, top_p=args.top_p, diagnostics=True)
+        fsel = fctx.select(q, k, v)
+        fctx.block_mass()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        m_hat, cap = fctx.block_mass()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        mp = fsel.block_prob.float()
+        x = mp.flatten(2) - mp.flatten(2).mean(-1, keepdim=True)
+        y = m_hat.flatten(2) - m_hat.flatten(2).mean(-1, keepdim=True)
+        r = (x * y).sum(-1) / (x.norm(dim=-1) * y.norm(dim=-1))
+        fidelity = {"block_mass_ms": e0.elapsed_time(e1), "captured_mass_mean": float(cap.mean()),
+                    "captured_mass_min_row": float(cap.min()), "pearson_r_mprime_mhat_mean": float(r.mean()),
+                    "pearson_r_min_head": float(r.min()), "random_selection_mass": fsel.kappa / fsel.n_k,
+                    "what": "m_hat = dense softmax mass per (sorted) block pair (ba_block_mass); captured = "
+                            "sum of m_hat over the selected blocks per query block"}
+        del fctx, fsel, m_hat, cap
+
     cpu = None
     if rank == 0 and not args.no_cpu and not args.profile and world == 1:
         hsel = 0
@@ -389,7 +417,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if heads else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": workload_desc(w, density, args.top_p), "global_batch": 1 if heads else world,
+            "config": {"workload": workload_desc(w, density, args.top_p, args.comp), "global_batch": 1 if heads else world,
                        "seq_len": w.seq_len,
                        "parallelism": (f"head-parallel x{world} (whole GQA groups per rank, NCCL all-gather of O)"
                                        if heads else f"batch-parallel x{world} (weak scaling, no data-path collective)"),
@@ -411,6 +439,8 @@ def run_ours(args):
             "tokens_per_s": tokens / (ms_per_step * 1e-3),
             "flops_per_step_per_rank": flops_per_step,
         }
+        if fidelity:
+            line["fidelity"] = fidelity
         line.update(res)
         print(json.dumps(line), flush=True)
     if world > 1:

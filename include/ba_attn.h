@@ -231,6 +231,21 @@ ba_status ba_attention_host(const ba_problem *prob, const ba_params *params,
                             void *out_host, void *workspace, size_t workspace_bytes,
                             cudaStream_t stream);
 
+/* NEXT-3 fidelity diagnostic: the oracle block distribution (Eq. oracle-dist,
+ * P:300-312) m_hat[g_q, g_k] = (1/|I(g_q)|) sum_{i in I(g_q)} sum_{j in J(g_k)}
+ * A_ij of the DENSE softmax A = softmax(Q' K'^T * scale) in the norm-sorted
+ * block space, and the selection's captured mass
+ * captured[g_q] = sum over the selected g_k of m_hat[g_q, g_k].
+ * Reads sel->q_sorted, k_sorted, v_sorted (and kv_index / kv_count when
+ * captured != NULL).  m_hat: [b, H_q, N_q, N_k] fp32; captured: [b, H_q, N_q]
+ * fp32 or NULL.  Runs a dense pass (for the row log-sum-exp) and a second
+ * S = Q'K'^T pass on the tensor cores.  bf16, head_dim 128, block_size 128
+ * (else BA_ERR_UNSUPPORTED).  workspace >= ba_block_mass_workspace_size. */
+size_t ba_block_mass_workspace_size(const ba_problem *prob, const ba_params *params);
+ba_status ba_block_mass(const ba_problem *prob, const ba_params *params, const ba_selection *sel,
+                        float *m_hat, float *captured, void *workspace, size_t workspace_bytes,
+                        cudaStream_t stream);
+
 /* Name of the attention kernel ba_sparse_attn / ba_attention / ba_dense_attn
  * run for this problem: "attn_sm100_tcgen05" (bf16, d = 128, B in {64, 128}:
  * tcgen05 tensor cores, TMA, TMEM; B = 64 pairs two query blocks per 128-row

@@ -82,6 +82,10 @@ def load() -> ctypes.CDLL:
     lib.ba_sparse_attn.restype = ctypes.c_int
     lib.ba_sparse_attn_gather.argtypes = [P, PA, vp, vp, vp, S, vp, vp, st]
     lib.ba_sparse_attn_gather.restype = ctypes.c_int
+    lib.ba_block_mass_workspace_size.argtypes = [P, PA]
+    lib.ba_block_mass_workspace_size.restype = sz
+    lib.ba_block_mass.argtypes = [P, PA, S, vp, vp, vp, sz, st]
+    lib.ba_block_mass.restype = ctypes.c_int
     lib.ba_zero_copy_supported.argtypes = [P, PA]
     lib.ba_zero_copy_supported.restype = ctypes.c_int
     lib.ba_attention.argtypes = [P, PA, vp, vp, vp, vp, vp, vp, sz, st]
@@ -102,7 +106,7 @@ def load() -> ctypes.CDLL:
 
 EXPORTED = ["ba_abi_version", "ba_selection_sizes", "ba_select_workspace_size", "ba_attention_workspace_size",
             "ba_select", "ba_sparse_attn", "ba_sparse_attn_gather", "ba_zero_copy_supported",
-            "ba_attention", "ba_dense_attn",
+            "ba_attention", "ba_dense_attn", "ba_block_mass_workspace_size", "ba_block_mass",
             "ba_attention_host_workspace_size", "ba_attention_host", "ba_last_launch_count",
             "ba_attention_kernel_name",
             "ba_status_string", "ba_last_error"]
@@ -283,6 +287,19 @@ class Context:
                                 ctypes.byref(self.sel_c), _ptr(self.ws_select), self.ws_select.numel(),
                                 _stream(stream)))
         return self.sel
+
+    def block_mass(self, captured: bool = True, stream=None):
+        """NEXT-3: (m_hat [b,Hq,Nq,Nk], captured [b,Hq,Nq]) of the dense softmax in the
+        sorted block space for the last selection (ba_block_mass)."""
+        lib = load()
+        q = self.qkv[0]
+        b, hq = q.shape[0], q.shape[1]
+        m_hat = torch.empty(b, hq, self.sel.n_q, self.sel.n_k, dtype=torch.float32, device=q.device)
+        cap = torch.empty(b, hq, self.sel.n_q, dtype=torch.float32, device=q.device) if captured else None
+        ws = _workspace(lib.ba_block_mass_workspace_size(ctypes.byref(self.prob), ctypes.byref(self.params)), q.device)
+        _check(lib.ba_block_mass(ctypes.byref(self.prob), ctypes.byref(self.params), ctypes.byref(self.sel_c),
+                                 _ptr(m_hat), _ptr(cap), _ptr(ws), ws.numel(), _stream(stream)))
+        return m_hat, cap
 
     def sparse_attn(self, out, lse=None, sel: Optional[Selection] = None, stream=None):
         sc = self.sel_c if sel is None else sel.to_c()

@@ -691,6 +691,54 @@ ba_status ba_attention_host(const ba_problem *prob, const ba_params *params, con
   return BA_OK;
 }
 
+// ---------------------------------------------------------------- NEXT-3 diagnostics
+size_t ba_block_mass_workspace_size(const ba_problem *prob, const ba_params *params) {
+  Dims D;
+  if (check_problem(prob, params, &D) != BA_OK) return 0;
+  return align_up(4ull * D.b * D.hq * D.lq) + align_up(D.esz * D.b * D.hq * D.lq * D.d);
+}
+
+ba_status ba_block_mass(const ba_problem *prob, const ba_params *params, const ba_selection *sel, float *m_hat,
+                        float *captured, void *workspace, size_t workspace_bytes, cudaStream_t stream) {
+  g_err.clear();
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  if (D.dtype != BA_DTYPE_BF16 || D.d != 128 || D.B != 128)
+    return fail(BA_ERR_UNSUPPORTED, "ba_block_mass: bf16, head_dim 128, block_size 128 (tcgen05 path)");
+  if (D.nk > 32 * 1024) return fail(BA_ERR_UNSUPPORTED, "ba_block_mass: N_k > 32768");
+  if (!sel || !sel->q_sorted || !sel->k_sorted || !sel->v_sorted)
+    return fail(BA_ERR_INVALID_ARGUMENT, "ba_block_mass reads sel->q_sorted/k_sorted/v_sorted");
+  if (!m_hat) return fail(BA_ERR_INVALID_ARGUMENT, "m_hat is NULL");
+  if (captured && (!sel->kv_index || !sel->kv_count))
+    return fail(BA_ERR_INVALID_ARGUMENT, "captured mass needs sel->kv_index/kv_count");
+  const size_t need = ba_block_mass_workspace_size(prob, params);
+  if (workspace_bytes < need) return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu < %zu", workspace_bytes, need);
+  if (!workspace) return fail(BA_ERR_INVALID_ARGUMENT, "workspace is NULL");
+  float *lse = at<float>(workspace, 0);
+  void *o_scratch = at<void>(workspace, align_up(4ull * D.b * D.hq * D.lq));
+  // 1. dense attention over the sorted copies: the row normaliser (LSE, sorted order)
+  AttnArgs a = make_attn(D, params);
+  a.q = sel->q_sorted; a.k = sel->k_sorted; a.v = sel->v_sorted;
+  a.qs[0] = D.hq * D.lq * D.d; a.qs[1] = D.lq * D.d; a.qs[2] = D.d;
+  a.ks[0] = D.hkv * D.lk * D.d; a.ks[1] = D.lk * D.d; a.ks[2] = D.d;
+  for (int i = 0; i < 3; ++i) { a.vs[i] = a.ks[i]; a.os[i] = a.qs[i]; }
+  a.kv_index = nullptr; a.kv_count = nullptr; a.kv_stride = D.nk; a.perm_q = nullptr;
+  a.out = o_scratch; a.lse = lse;
+  BA_TRY(run_attn(a, stream));
+  // 2. S again, exp(S*scale - lse) reduced per (query block, key block)
+  MassArgs m{};
+  m.d = (int)D.d; m.B = (int)D.B;
+  m.batch = D.b; m.hq = D.hq; m.hkv = D.hkv; m.lq = D.lq; m.lk = D.lk; m.nq = D.nq; m.nk = D.nk;
+  m.q = sel->q_sorted; m.k = sel->k_sorted;
+  for (int i = 0; i < 3; ++i) { m.qs[i] = a.qs[i]; m.ks[i] = a.ks[i]; }
+  m.lse = lse; m.scale = a.scale;
+  m.kv_index = sel->kv_index; m.kv_count = sel->kv_count; m.kv_stride = D.kappa;
+  m.m_hat = m_hat; m.captured = captured;
+  BA_TRY(cuda_check(launch_block_mass(m, stream), "block_mass"));
+  g_launches = 2;
+  return BA_OK;
+}
+
 int ba_last_launch_count(void) { return g_launches; }
 
 const char *ba_attention_kernel_name(const ba_problem *prob, const ba_params *params) {

@@ -91,4 +91,22 @@ bool attn_2cta_supported(const AttnArgs &a);
 cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st);
 bool attn_pp_supported(const AttnArgs &a);
 
+// ---------------------------------------------------------------- NEXT-3: oracle block mass
+struct MassArgs {
+  int d, B;
+  int64_t batch, hq, hkv, lq, lk, nq, nk;
+  const void *q, *k;            // Q', K' (sorted copies), bf16
+  int64_t qs[3], ks[3];
+  const float *lse;             // [b, hq, lq] natural-log row LSE of the dense softmax, sorted order
+  float scale;
+  const int32_t *kv_index;      // selection for the captured mass (or nullptr)
+  const int32_t *kv_count;
+  int64_t kv_stride;
+  float *m_hat;                 // [b, hq, nq, nk]
+  float *captured;              // [b, hq, nq] or nullptr
+};
+bool block_mass_supported(const MassArgs &a);
+cudaError_t launch_block_mass(const MassArgs &a, cudaStream_t st);
+
 }  // namespace baatt
+

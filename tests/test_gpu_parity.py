@@ -407,3 +407,51 @@ def test_selection_exact_compensation(ba, cfg, L, hq, hkv, B, dens, beta):
     diag = oracle_select_all(q, k, B, dens, beta, "qk", "diag")
     assert any(np.abs(ref[kk].m - diag[kk].m).max() > 1e-9 for kk in ref)
     assert max_abs_err(out, oracle_output_with_gpu_selection(q, k, v, sel, B)) <= TOL[q.dtype]
+
+
+# ---------------------------------------------------------------- NEXT-3: oracle block distribution on the GPU
+@pytest.mark.parametrize("cfg,L,hq,hkv,dens", [("A", 2048 + 77, 2, 2, 0.5), ("C", 1024 * 3, 4, 1, 0.25), ("V", 128 * 9 + 80, 2, 2, 0.5)])
+def test_block_mass_matches_oracle(ba, cfg, L, hq, hkv, dens):
+    """ba_block_mass: m_hat (Eq. oracle-dist) of the dense softmax in the
+    sorted block space vs the fp64 oracle's oracle_block_mass(dense map), and the
+    selection's captured mass.  Tolerance: S is an fp32 sum of exact bf16 products
+    (relative error ~1e-6 |S|), exp2 / LSE in fp32: |dm_hat| <= 3e-5 + 1e-3 m_hat."""
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv)
+    ctx = ba.Context(q, k, v, 128, dens)
+    sel = ctx.select(q, k, v)
+    m_hat, cap = ctx.block_mass()
+    torch.cuda.synchronize()
+    mh = m_hat.double().cpu().numpy()
+    cp = cap.double().cpu().numpy()
+    pq, pk, idx, cnt = (sel.perm_q.cpu().numpy(), sel.perm_k.cpu().numpy(), sel.kv_index.cpu().numpy(),
+                        sel.kv_count.cpu().numpy())
+    grp = hq // hkv
+    for h in range(hq):
+        Qs = O.apply_permutation(q[0, h].cpu(), pq[0, h])
+        Ks = O.apply_permutation(k[0, h // grp].cpu(), pk[0, h // grp])
+        ref = O.oracle_block_mass(O.dense_attention_map(Qs, Ks), 128, 128)
+        np.testing.assert_allclose(mh[0, h], ref, atol=3e-5, rtol=1e-3)
+        np.testing.assert_allclose(mh[0, h].sum(1), 1.0, atol=1e-4)
+        ref_cap = np.array([ref[g, idx[0, h, g, :cnt[0, h, g]]].sum() for g in range(ref.shape[0])])
+        np.testing.assert_allclose(cp[0, h], ref_cap, atol=1e-4, rtol=1e-3)
+
+
+def test_block_mass_fullsize_properties(ba):
+    """Config A, one head at full length (32K): rows of m_hat sum to 1, the
+    selection's captured mass never exceeds the greedy optimum (top-kappa of
+    m_hat itself), and the selection captures more mass than kappa
+    blocks chosen at random would on average (kappa / N_k)."""
+    w = CONFIGS["A"]
+    q, k, v = make_qkv(w, device="cuda", heads_q=1, heads_kv=1)
+    ctx = ba.Context(q, k, v, 128, 0.5)
+    sel = ctx.select(q, k, v)
+    m_hat, cap = ctx.block_mass()
+    torch.cuda.synchronize()
+    mh = m_hat[0, 0].double()
+    assert torch.allclose(mh.sum(1), torch.ones_like(mh[:, 0]), atol=1e-3)
+    kap = sel.kappa
+    greedy = torch.topk(mh, kap, dim=1).values.sum(1)
+    c = cap[0, 0].double()
+    assert (c <= greedy + 1e-4).all()
+    assert c.mean() > kap / sel.n_k + 0.05
