@@ -18,10 +18,13 @@
 // during each softmax (FA4-style ping-pong) and 32 MMAs per K/V wait; each
 // softmax warpgroup owns whole rows (no cross-warp max exchange).
 //
-// Warps: 0 TMA producer (Q_A, Q_B once; then K_u, V_u into a 2-stage ring),
-//        1 MMA issuer (one elected thread) + TMEM owner,
-//        2-5 softmax of block A, 6-9 softmax of block B (one thread per row,
-//        128 columns).
+// Warps: 0-3 softmax of block A, 4-7 softmax of block B (one thread per row,
+//        128 columns; warp w reads TMEM lane quadrant w % 4),
+//        8 TMA producer (Q_A, Q_B once; then K_u, V_u into a 5-slot ring),
+//        9 MMA issuer (one elected thread) + TMEM owner, 10-11 idle.
+//        setmaxnreg moves registers from warpgroup 2 (warps 8-11: 80 each) to
+//        the softmax warpgroups (208 each): a 128-column S row per thread and
+//        the exp-offload polynomial fit without spills.
 // TMEM: S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).
 // Issue order per union tile u:
 //   PV_A(u-1) | S_A(u) | PV_B(u-1) | S_B(u)      (softmax A(u) || PV_B, S_B)
@@ -55,7 +58,9 @@ constexpr uint32_t TILE = 2 * BOX;           // 128 x 128 bf16 (32 KB)
 constexpr int NSLOT = 5;
 BA_DEVICE constexpr uint32_t s_col(int x) { return x ? 128u : 0u; }
 constexpr uint32_t O_COL0 = 256;
-constexpr int kThreads = 320;
+constexpr int kProducerWarp = 8, kMmaWarp = 9;
+constexpr int kThreads = 384;             // 12 warps: 8 softmax (warpgroups 0, 1) + warpgroup 2 (producer, MMA, 2 idle)
+constexpr int kRegsSoftmax = 208, kRegsSide = 80;  // setmaxnreg: 8*32*208 + 4*32*80 = 63488 <= 65536
 constexpr float kRescaleThreshold = 8.0f;
 constexpr int kMaskWords = 256;                             // nk <= 8192 (L <= 1M tokens)
 constexpr int kTraceTiles = 8;
@@ -171,7 +176,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       tma_prefetch(&tm_v);
     }
   }
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&bars.tmem_base)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -181,7 +186,11 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
   const uint32_t tmem = bars.tmem_base;
   const int cnt = (int)bars.n_union;
 
-  if (warp == 0) {
+  if (warp >= 8) {
+  // warpgroup 2 gives registers to the softmax warpgroups (each softmax thread holds a
+  // 128-column S row); setmaxnreg is warpgroup-collective, so the role branches nest here
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsSide));
+  if (warp == kProducerWarp) {
     // ================================================================ TMA producer
     // tile loads of the permuted copies by lane 0, or (kGather bits) tile::gather4 of the
     // original rows through pi by all 32 lanes, lane l fetching rows 4l..4l+3 of each tile
@@ -255,7 +264,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ================================================================ MMA issuer
     if (lane == 0 && cnt > 0) {
       mbar_wait(&bars.q_full, 0);
@@ -308,9 +317,11 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       mma_commit(&bars.o_final);
     }
     __syncwarp();
-  } else if (warp >= 2 && warp < 10) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
     // ================================================================ softmax + epilogue
-    const int x = (warp - 2) >> 2;      // 0: block A, 1: block B
+    const int x = warp >> 2;            // 0: block A, 1: block B
     const int qd = warp & 3;            // TMEM lane quadrant
     const int r = qd * 32 + lane;       // row within the query block
     const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
@@ -340,7 +351,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     for (int u = 0; u < cnt; ++u) {
       const int gk = walk.next();
       const bool mine = (my_mask[gk >> 5] >> (gk & 31)) & 1u;  // warpgroup-uniform
-      const bool trx = kTrace && (warp == 2 || warp == 6) && lane == 0;
+      const bool trx = kTrace && (warp == 0 || warp == 4) && lane == 0;
       mbar_wait(&bars.s_full[x], (uint32_t)u & 1u);
       if (trx) TR(4 + 4 * x, u);
       tc_fence_after();
@@ -459,7 +470,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     }
   }
 #undef TR
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
@@ -518,18 +529,27 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
     if (dbg < 0 || dbg > 2) dbg = 0;
     const char *e = getenv("BA_EXP_EMU");
     emu = e ? atoi(e) : kDefaultEmu;
-    if (emu < 0 || emu > 3) emu = kDefaultEmu;
+    if (emu < 0 || emu > 5) emu = kDefaultEmu;
   }
   dim3 grid((unsigned)((a.nq + 1) / 2), (unsigned)(a.batch * a.hq));
   if (dbg == 1) return launch_mode<1, 0>(a, mq, mk, mv, grid, st);
   if (dbg == 2) return stagger ? launch_mode<2, kDefaultEmu>(a, mq, mk, mv, grid, st)
                                : launch_mode<2, kDefaultEmu, false>(a, mq, mk, mv, grid, st);
-  if (!stagger) return launch_mode<0, kDefaultEmu, false>(a, mq, mk, mv, grid, st);
-  switch (emu) {
-    case 0: return launch_mode<0, 0>(a, mq, mk, mv, grid, st);
-    case 1: return launch_mode<0, 1>(a, mq, mk, mv, grid, st);
-    case 2: return launch_mode<0, 2>(a, mq, mk, mv, grid, st);
-    default: return launch_mode<0, 3>(a, mq, mk, mv, grid, st);
+  if (stagger) {
+    switch (emu) {
+      case 0: return launch_mode<0, 0, true>(a, mq, mk, mv, grid, st);
+      case 1: return launch_mode<0, 1, true>(a, mq, mk, mv, grid, st);
+      case 2: return launch_mode<0, 2, true>(a, mq, mk, mv, grid, st);
+      default: return launch_mode<0, 3, true>(a, mq, mk, mv, grid, st);
+    }
+  }
+  switch (emu) {  // of every 8 exp2 pairs, emu go to the FMA-pipe polynomial
+    case 0: return launch_mode<0, 0, false>(a, mq, mk, mv, grid, st);
+    case 1: return launch_mode<0, 1, false>(a, mq, mk, mv, grid, st);
+    case 2: return launch_mode<0, 2, false>(a, mq, mk, mv, grid, st);
+    case 3: return launch_mode<0, 3, false>(a, mq, mk, mv, grid, st);
+    case 4: return launch_mode<0, 4, false>(a, mq, mk, mv, grid, st);
+    default: return launch_mode<0, 5, false>(a, mq, mk, mv, grid, st);
   }
 }
 

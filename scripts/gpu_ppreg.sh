@@ -1,0 +1,9 @@
+# pair kernel with setmaxnreg (12 warps): parity, exp-offload sweep, trace
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider --timeout 300 -o timeout_method=thread -k "pp or zero_copy or B64 or bf16_full" 2>&1 | tail -2
+for cfg in A C; do
+for mode in "BA_EXP_EMU=0" "BA_EXP_EMU=1" "BA_EXP_EMU=2" "BA_EXP_EMU=3" "BA_ATTN_DEBUG=1"; do
+  env $mode timeout 200 python bench.py --config $cfg --steps 5 --warmup 3 --no-e2e --no-cpu --no-dense > gpurun_out/p.json 2>gpurun_out/p.err
+  python -c "import json;d=json.load(open('gpurun_out/p.json'));print('$cfg $mode',d['roofline']['kernel'],'attn',round(d['roofline']['achieved'],1),'value',round(d['value'],1),'clk',(d['clocks'] or {}).get('sm_mhz'),(d['clocks'] or {}).get('reasons'))" 2>&1 | tail -1
+  tail -1 gpurun_out/p.err
+done; done
+BA_ATTN_DEBUG=2 timeout 200 python bench.py --config A --steps 1 --warmup 0 --no-e2e --no-cpu --no-dense 2>&1 | grep TRACE | head -12
