@@ -291,7 +291,7 @@ AttnArgs make_attn(const Dims &D, const ba_params *pa) {
 // default: +1.5-2% over 1cta on A and C), "2cta" (cluster pair,
 // attn_sm100_2cta.cu) or "1cta" (attn_sm100.cu).  The pair kernels walk the
 // union of two adjacent query blocks' lists.
-enum K5Kind { K5_1CTA = 0, K5_2CTA = 1, K5_PP = 2 };
+enum K5Kind { K5_1CTA = 0, K5_2CTA = 1, K5_PP = 2, K5_PPS = 3 };
 static const int kDefaultK5 = K5_PP;
 
 static int k5_kind() {
@@ -300,6 +300,7 @@ static int k5_kind() {
     kind = kDefaultK5;
     const char *env = getenv("BA_ATTN_K5");
     if (env && !strcmp(env, "pp")) kind = K5_PP;
+    else if (env && !strcmp(env, "pps")) kind = K5_PPS;
     else if (env && !strcmp(env, "2cta")) kind = K5_2CTA;
     else if (env && !strcmp(env, "1cta")) kind = K5_1CTA;
     else if (getenv("BA_ATTN_2CTA") && atoi(getenv("BA_ATTN_2CTA"))) kind = K5_2CTA;
@@ -307,10 +308,12 @@ static int k5_kind() {
   return kind;
 }
 
-bool use_pp(const AttnArgs &a) { return k5_kind() == K5_PP && attn_pp_supported(a); }
+bool use_pps(const AttnArgs &a) { return k5_kind() == K5_PPS && attn_pps_supported(a); }
+bool use_pp(const AttnArgs &a) { return (k5_kind() == K5_PP || (k5_kind() == K5_PPS && !attn_pps_supported(a))) && attn_pp_supported(a); }
 bool use_2cta(const AttnArgs &a) { return k5_kind() == K5_2CTA && attn_2cta_supported(a); }
 
 const char *attn_kernel_name(const AttnArgs &a) {
+  if (use_pps(a)) return "attn_sm100_tcgen05_pps";
   if (use_pp(a)) return "attn_sm100_tcgen05_pp";
   if (use_2cta(a)) return "attn_sm100_tcgen05_2cta";
   if (!attn_sm100_supported(a)) return "attn_simt";
@@ -319,7 +322,8 @@ const char *attn_kernel_name(const AttnArgs &a) {
 
 ba_status run_attn(const AttnArgs &a, cudaStream_t st) {
   cudaError_t e;
-  if (use_pp(a)) e = launch_attn_pp(a, st);
+  if (use_pps(a)) e = launch_attn_pps(a, st);
+  else if (use_pp(a)) e = launch_attn_pp(a, st);
   else if (use_2cta(a)) e = launch_attn_2cta(a, st);
   else if (attn_sm100_supported(a)) e = launch_attn_sm100(a, st);
   else e = launch_attn_simt(a, st);

@@ -64,7 +64,7 @@ constexpr int kRegsSoftmax = 208, kRegsSide = 80;  // setmaxnreg: 8*32*208 + 4*3
 constexpr float kRescaleThreshold = 8.0f;
 constexpr int kMaskWords = 256;                             // nk <= 8192 (L <= 1M tokens)
 constexpr int kTraceTiles = 8;
-constexpr int kDefaultEmu = 0;
+constexpr int kDefaultEmu = 1;  // 1 of 8 exp2 pairs on the FMA pipe: +2.4% at A, +1.4% at C (EMU sweep, profiles/round1_microbench.txt)
 constexpr uint32_t SMEM_Q = 0;                              // Q_A, Q_B
 constexpr uint32_t SMEM_SLOT = 2 * TILE;
 constexpr uint32_t SMEM_MASK = SMEM_SLOT + NSLOT * TILE;

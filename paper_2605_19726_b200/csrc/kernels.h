@@ -90,6 +90,8 @@ cudaError_t launch_attn_2cta(const AttnArgs &a, cudaStream_t st);
 bool attn_2cta_supported(const AttnArgs &a);
 cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st);
 bool attn_pp_supported(const AttnArgs &a);
+cudaError_t launch_attn_pps(const AttnArgs &a, cudaStream_t st);
+bool attn_pps_supported(const AttnArgs &a);
 
 // ---------------------------------------------------------------- NEXT-3: oracle block mass
 struct MassArgs {

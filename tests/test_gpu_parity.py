@@ -182,7 +182,7 @@ def test_injected_oracle_mask(ba):
     assert ref_sel  # oracle selection computed on the same inputs
 
 
-@pytest.mark.parametrize("B,k5", [(128, "1cta"), (128, "2cta"), (128, "pp"), (64, "dual"), (64, "pair")])
+@pytest.mark.parametrize("B,k5", [(128, "1cta"), (128, "2cta"), (128, "pp"), (128, "pps"), (64, "dual"), (64, "pair")])
 def test_injected_dissimilar_lists(ba, B, k5):
     """Random (dissimilar) index lists for every query block: exercises the
     pair kernels' union walk where a block skips tiles (P = 0 rows), including
@@ -241,7 +241,7 @@ def test_errors_are_loud(ba):
 
 
 @pytest.mark.parametrize("k5,name", [("2cta", "attn_sm100_tcgen05_2cta"), ("pp", "attn_sm100_tcgen05_pp"),
-                                     ("1cta", "attn_sm100_tcgen05")])
+                                     ("pps", "attn_sm100_tcgen05_pps"), ("1cta", "attn_sm100_tcgen05")])
 def test_b128_kernel_parity(ba, k5, name):
     """Each B = 128 kernel (BA_ATTN_K5 = 2cta | pp | 1cta) on real selections,
     ragged lengths, GQA and an odd number of query blocks."""
