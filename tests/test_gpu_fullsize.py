@@ -42,29 +42,37 @@ def _blocks_to_check(ref, nq, seed):
     return sorted({0, nq - 1, int(near.argmax()), int(rng.integers(nq))})
 
 
-@pytest.mark.parametrize("cfg,density", [("A", 0.5), ("C", 0.5), ("C", 0.25), ("V", 0.5), ("M", 0.5)])
-def test_fullsize(ba, cfg, density):
+@pytest.mark.parametrize("cfg,density,top_p", [("A", 0.5, None), ("C", 0.5, None), ("C", 0.25, None), ("V", 0.5, None),
+                                              ("M", 0.5, None), ("C", 1.0, 0.9), ("M", 0.5, 0.95)])
+def test_fullsize(ba, cfg, density, top_p):
     w = CONFIGS[cfg]
     torch.cuda.empty_cache()
     q, k, v = make_qkv(w, device="cuda")
-    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag")
+    if top_p is not None:
+        top_p = float(np.float32(top_p))  # the ABI carries top_p as fp32
+    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", "diag", top_p=top_p)
     out = torch.empty_like(q)
     sel = ctx.select(q, k, v)
     ctx.sparse_attn(out)
     torch.cuda.synchronize()
     kappa, nq, nk = sel.kappa, sel.n_q, sel.n_k
     # ---- properties over the whole problem
-    assert (sel.kv_count == kappa).all()
+    cnt = sel.kv_count.long()
+    if top_p is None:
+        assert (cnt == kappa).all()
+    else:
+        assert (cnt >= 1).all() and (cnt <= kappa).all()
     idx = sel.kv_index.long()
-    assert (idx >= 0).all() and (idx < nk).all()
-    assert (idx[..., 1:] > idx[..., :-1]).all()
+    valid = torch.arange(kappa, device="cuda") < cnt[..., None]
+    assert ((idx >= 0) & (idx < nk) | ~valid).all()
+    assert ((idx[..., 1:] > idx[..., :-1]) | ~valid[..., 1:]).all()
     assert torch.isfinite(out.float()).all()
     for perm in (sel.perm_q, sel.perm_k):
         srt = torch.sort(perm.long(), dim=-1).values
         assert torch.equal(srt, torch.arange(perm.shape[-1], device="cuda").expand_as(srt))
     # ---- selection of sampled heads vs the oracle (every query block)
     heads = sorted({0, w.heads_q - 1})
-    ref = oracle_select_all(q, k, w.block_size, density, 1.0, "qk", "diag", heads=heads)
+    ref = oracle_select_all(q, k, w.block_size, density, 1.0, "qk", "diag", heads=heads, top_p=top_p)
     rep = check_selection(sel, ref)
     # ---- sampled output blocks vs the oracle (GPU perm + index lists)
     grp = w.heads_q // w.heads_kv
@@ -74,7 +82,9 @@ def test_fullsize(ba, cfg, density):
         hk = h // grp
         pq = sel.perm_q[0, h].cpu().numpy()
         pk = sel.perm_k[0, hk].cpu().numpy()
-        kvi = sel.kv_index[0, h].cpu().numpy()
+        kvi_all = sel.kv_index[0, h].cpu().numpy()
+        kvc = sel.kv_count[0, h].cpu().numpy()
+        kvi = [kvi_all[g, :kvc[g]] for g in range(nq)]
         Qs = O.apply_permutation(q[0, h].cpu(), pq)
         Ks = O.apply_permutation(k[0, hk].cpu(), pk)
         Vs = O.apply_permutation(v[0, hk].cpu(), pk)
