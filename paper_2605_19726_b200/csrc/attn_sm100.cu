@@ -57,6 +57,7 @@ constexpr int kVProducerWarp = 10;
 constexpr int kThreads = 352;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kDefaultEmu = 0;             // pairs per 8 on the polynomial exp2 (off: MUFU + power cap wins)
+constexpr int kDefaultEmu64 = 1;           // dual-tile (B = 64) kernel
 constexpr int kMaskWords = 1024;           // bitmask capacity: N_k <= 32768 key blocks
 
 template <int kBN>
@@ -622,9 +623,11 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
     return cudaErrorInvalidValue;
   // exp2 offload fraction: compile-time variants, BA_EXP_EMU=0..2 selects one (tuning knob);
   // BA_ATTN_DEBUG=1 / 2 select the no-softmax / trace profiling variants (B = 128)
-  static int emu = -1, dbg = -1;
+  static int emu = -1, dbg = -1, emu64 = -1;
   const int b64 = attn_sm100_dual64() ? 1 : 0;
   if (emu < 0) {
+    const char *e64 = getenv("BA_EXP_EMU");
+    emu64 = e64 ? atoi(e64) : kDefaultEmu64;
     const char *env = getenv("BA_EXP_EMU");
     emu = env ? atoi(env) : kDefaultEmu;
     if (emu < 0 || emu > 2) emu = kDefaultEmu;
@@ -639,7 +642,11 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
       b2.dbg_flags = sk ? atoi(sk) : 0;
       return launch_variant<128, 0, true, false, true>(b2, mk, mv, st);
     }
-    return launch_variant<128, 0, false, false, true>(a, mk, mv, st);
+    switch (emu64) {  // exp2 offload for the dual-tile kernel (BA_EXP_EMU; default kDefaultEmu64)
+      case 0: return launch_variant<128, 0, false, false, true>(a, mk, mv, st);
+      case 2: return launch_variant<128, 2, false, false, true>(a, mk, mv, st);
+      default: return launch_variant<128, 1, false, false, true>(a, mk, mv, st);
+    }
   }
   if (dbg == 1) {
     AttnArgs b2 = a;
