@@ -777,7 +777,8 @@ cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t
   // 128-tiles (16 warps) unless that leaves under ~2 CTAs per SM; BA_SCORES_SIMT=1 selects
   // the SIMT DFMA kernel (A/B profiling knob)
   const int64_t big = ((nk + 127) / 128) * ((nq + 127) / 128) * batch * hq;
-  const int tile = big >= 2 * 148 ? 128 : 64;
+  static const int tile_min = getenv("BA_SCORES_TILE128_MIN") ? atoi(getenv("BA_SCORES_TILE128_MIN")) : 2 * 148;
+  const int tile = big >= tile_min ? 128 : 64;
   static int simt = -1;
   if (simt < 0) simt = getenv("BA_SCORES_SIMT") ? atoi(getenv("BA_SCORES_SIMT")) : 0;
   dim3 grid((unsigned)((nk + tile - 1) / tile), (unsigned)((nq + tile - 1) / tile), (unsigned)(batch * hq));
