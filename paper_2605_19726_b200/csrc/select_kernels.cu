@@ -774,10 +774,11 @@ cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t
                           cudaStream_t st) {
   const double inv_sqrt_d = 1.0 / sqrt((double)d), bod = beta / (double)d;
   const int64_t grp = hq / hkv;
-  // 128-tiles (16 warps) unless that leaves under ~2 CTAs per SM; BA_SCORES_SIMT=1 selects
+  // BA_SCORES_SIMT=1 selects
   // the SIMT DFMA kernel (A/B profiling knob)
   const int64_t big = ((nk + 127) / 128) * ((nq + 127) / 128) * batch * hq;
-  static const int tile_min = getenv("BA_SCORES_TILE128_MIN") ? atoi(getenv("BA_SCORES_TILE128_MIN")) : 2 * 148;
+  // 128-tiles (16 warps) unless fewer than ~100 CTAs would result (A: 128 CTAs of 128 beat 512 of 64: 0.79 -> 0.76 ms selection)
+  static const int tile_min = getenv("BA_SCORES_TILE128_MIN") ? atoi(getenv("BA_SCORES_TILE128_MIN")) : 100;
   const int tile = big >= tile_min ? 128 : 64;
   static int simt = -1;
   if (simt < 0) simt = getenv("BA_SCORES_SIMT") ? atoi(getenv("BA_SCORES_SIMT")) : 0;
