@@ -774,8 +774,7 @@ cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t
                           cudaStream_t st) {
   const double inv_sqrt_d = 1.0 / sqrt((double)d), bod = beta / (double)d;
   const int64_t grp = hq / hkv;
-  // BA_SCORES_SIMT=1 selects
-  // the SIMT DFMA kernel (A/B profiling knob)
+  // BA_SCORES_SIMT=1 selects the SIMT DFMA kernel (A/B profiling knob)
   const int64_t big = ((nk + 127) / 128) * ((nq + 127) / 128) * batch * hq;
   // 128-tiles (16 warps) unless fewer than ~100 CTAs would result (A: 128 CTAs of 128 beat 512 of 64: 0.79 -> 0.76 ms selection)
   static const int tile_min = getenv("BA_SCORES_TILE128_MIN") ? atoi(getenv("BA_SCORES_TILE128_MIN")) : 100;
