@@ -97,3 +97,33 @@ def test_fullsize(ba, cfg, density, top_p):
             err = np.abs(gout[rows] - Os[s:e]).max()
             worst = max(worst, float(err))
     assert worst <= TOL[q.dtype], (worst, rep)
+
+
+def test_max_length_one_million_tokens(ba):
+    """Maximum size of the pair kernel's bitmask (N_k = 8192 key blocks: L = 2^20
+    tokens, B = 128), 5% density: selection of the head vs the oracle (every
+    query block, within the band), sampled output blocks vs the oracle, and the
+    whole-problem properties."""
+    w = CONFIGS["A"]
+    L = 1 << 20
+    torch.cuda.empty_cache()
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=1, heads_kv=1)
+    assert ba.attention_kernel_name(q, k, v, 128) == "attn_sm100_tcgen05_pp"
+    ctx = ba.Context(q, k, v, 128, 0.05)
+    sel = ctx.select(q, k, v)
+    out = torch.empty_like(q)
+    ctx.sparse_attn(out)
+    torch.cuda.synchronize()
+    assert sel.n_k == 8192 and (sel.kv_count == sel.kappa).all()
+    assert torch.isfinite(out.float()).all()
+    ref = oracle_select_all(q, k, 128, 0.05, 1.0, "qk", "diag")
+    check_selection(sel, ref)
+    pq, pk = sel.perm_q[0, 0].cpu().numpy(), sel.perm_k[0, 0].cpu().numpy()
+    kvi = sel.kv_index[0, 0].cpu().numpy()
+    Qs, Ks, Vs = (O.apply_permutation(t[0, 0].cpu(), p) for t, p in ((q, pq), (k, pk), (v, pk)))
+    blocks = _blocks_to_check(ref[(0, 0)], sel.n_q, seed=7)
+    Os, _ = O.block_sparse_attention_head(Qs, Ks, Vs, kvi, 128, 1.0 / math.sqrt(128), blocks)
+    gout = out[0, 0].float().cpu().numpy()
+    for g in blocks:
+        rows = pq[g * 128:(g + 1) * 128]
+        assert np.abs(gout[rows] - Os[g * 128:(g + 1) * 128]).max() <= TOL[q.dtype]
