@@ -605,22 +605,6 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
   using namespace sm100;
   CUtensorMap mk, mv;
   if (!get_encode()) return cudaErrorNotSupported;  // no TMA encoder: fail loudly, never fall back
-  if (a.gather) {  // zero-copy: B = 128 single-block tiles, or B = 64 dual tiles
-    if (a.B == 64 && !attn_sm100_dual64()) return cudaErrorNotSupported;
-    if (a.gather & 2) {
-      if (!make_gather_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) || !make_gather_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs))
-        return cudaErrorInvalidValue;
-      if (a.B == 64) return launch_variant<128, 0, false, false, true, 3>(a, mk, mv, st);
-      return launch_variant<128, 0, false, false, false, 3>(a, mk, mv, st);
-    }
-    if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, a.B) || !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, a.B))
-      return cudaErrorInvalidValue;
-    if (a.B == 64) return launch_variant<128, 0, false, false, true, 1>(a, mk, mv, st);
-    return launch_variant<128, 0, false, false, false, 1>(a, mk, mv, st);
-  }
-  if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, a.B) ||
-      !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, a.B))
-    return cudaErrorInvalidValue;
   // exp2 offload fraction: compile-time variants, BA_EXP_EMU=0..2 selects one (tuning knob);
   // BA_ATTN_DEBUG=1 / 2 select the no-softmax / trace profiling variants (B = 128)
   static int emu = -1, dbg = -1, emu64 = -1;
@@ -628,12 +612,43 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
   if (emu < 0) {
     const char *e64 = getenv("BA_EXP_EMU");
     emu64 = e64 ? atoi(e64) : kDefaultEmu64;
+    if (emu64 < 0 || emu64 > 2) emu64 = kDefaultEmu64;
     const char *env = getenv("BA_EXP_EMU");
     emu = env ? atoi(env) : kDefaultEmu;
     if (emu < 0 || emu > 2) emu = kDefaultEmu;
     const char *d = getenv("BA_ATTN_DEBUG");
     dbg = d ? atoi(d) : 0;
   }
+  if (a.gather) {  // zero-copy: B = 128 single-block tiles, or B = 64 dual tiles
+    if (a.B == 64 && !attn_sm100_dual64()) return cudaErrorNotSupported;
+    // same exp2-offload variant as the copy path, so both paths are bit-identical
+    const int e = a.B == 64 ? emu64 : emu;
+    if (a.gather & 2) {
+      if (!make_gather_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) || !make_gather_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs))
+        return cudaErrorInvalidValue;
+      if (a.B == 64) {
+        if (e == 0) return launch_variant<128, 0, false, false, true, 3>(a, mk, mv, st);
+        if (e == 2) return launch_variant<128, 2, false, false, true, 3>(a, mk, mv, st);
+        return launch_variant<128, 1, false, false, true, 3>(a, mk, mv, st);
+      }
+      if (e == 1) return launch_variant<128, 1, false, false, false, 3>(a, mk, mv, st);
+      if (e == 2) return launch_variant<128, 2, false, false, false, 3>(a, mk, mv, st);
+      return launch_variant<128, 0, false, false, false, 3>(a, mk, mv, st);
+    }
+    if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, a.B) || !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, a.B))
+      return cudaErrorInvalidValue;
+    if (a.B == 64) {
+      if (e == 0) return launch_variant<128, 0, false, false, true, 1>(a, mk, mv, st);
+      if (e == 2) return launch_variant<128, 2, false, false, true, 1>(a, mk, mv, st);
+      return launch_variant<128, 1, false, false, true, 1>(a, mk, mv, st);
+    }
+    if (e == 1) return launch_variant<128, 1, false, false, false, 1>(a, mk, mv, st);
+    if (e == 2) return launch_variant<128, 2, false, false, false, 1>(a, mk, mv, st);
+    return launch_variant<128, 0, false, false, false, 1>(a, mk, mv, st);
+  }
+  if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, a.B) ||
+      !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, a.B))
+    return cudaErrorInvalidValue;
   if (a.B == 64) {
     if (b64 == 0) return launch_variant<64, 0, false, false>(a, mk, mv, st);
     if (dbg == 1) {

@@ -79,7 +79,7 @@ constexpr uint32_t IDESC_O = IDESC_S | (1u << 16);  // B = V MN-major (N = d = 1
 struct __align__(8) Bars {
   uint64_t q_full;
   uint64_t full[NSLOT], empty[NSLOT];
-  uint64_t s_full[2], p_full[2];  // per query block (A, B)
+  uint64_t s_full[2], p_half[2], p_full[2];  // per query block (A, B); p_half: P keys 0-63 in TMEM
   uint64_t tok[2][4];             // MUFU token per SMSP: softmax A(u) -> B(u) -> A(u+1) ...
   uint64_t o_final;
   uint32_t tmem_base;
@@ -167,7 +167,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       bars.last_ragged = sel_last && (a.lk - gl * (int64_t)BN) < BN;
       mbar_init(&bars.q_full, 1);
       for (int s = 0; s < NSLOT; ++s) { mbar_init(&bars.full[s], 1); mbar_init(&bars.empty[s], 1); }
-      for (int s = 0; s < 2; ++s) { mbar_init(&bars.s_full[s], 1); mbar_init(&bars.p_full[s], 4); }
+      for (int s = 0; s < 2; ++s) { mbar_init(&bars.s_full[s], 1); mbar_init(&bars.p_half[s], 4); mbar_init(&bars.p_full[s], 4); }
       for (int s = 0; s < 8; ++s) mbar_init(&bars.tok[s >> 2][s & 3], 1);
       mbar_init(&bars.o_final, 1);
       fence_barrier_init();
@@ -282,10 +282,12 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         }
         mma_commit(&bars.s_full[x]);
       };
-      auto issue_pv = [&](int x, int u) {  // O_x += P_x V_u, P_x read from TMEM
+      // O_x += P_x V_u, P_x read from TMEM, in two halves of 64 keys: the first half is issued
+      // as soon as the softmax has stored P for keys 0-63 (p_half), overlapping its second half
+      auto issue_pv = [&](int x, int u, int h) {
         const uint32_t sv = slot_addr(2 * u + 1);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
+        for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
           mma_ts(tmem + O_COL0 + 128 * x, tmem + s_col(x) + kk * 8, make_desc(sv + kk * 2048, BOX, 1024), IDESC_O,
                  (u > 0 || kk > 0) ? 1u : 0u);
       };
@@ -295,19 +297,25 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       mma_commit(&bars.empty[0]);  // K_0 read by both
       for (int u = 0; u < cnt; ++u) {
         const bool next = u + 1 < cnt;
-        mbar_wait(&bars.p_full[0], (uint32_t)u & 1u);  // softmax A wrote P_A(u)
+        mbar_wait(&bars.p_half[0], (uint32_t)u & 1u);  // softmax A wrote P_A(u), keys 0-63
         TR(1, u);
         wait_full(2 * u + 1);
-        issue_pv(0, u);
+        issue_pv(0, u, 0);
+        mbar_wait(&bars.p_full[0], (uint32_t)u & 1u);  // ... and keys 64-127
+        tc_fence_after();
+        issue_pv(0, u, 1);
         if (next) {
           wait_full(2 * u + 2);
           issue_s(0, u + 1);  // S_A buffer reuse: after PV_A(u) in issue order
           TR(2, u + 1);
         }
-        mbar_wait(&bars.p_full[1], (uint32_t)u & 1u);  // softmax B wrote P_B(u)
+        mbar_wait(&bars.p_half[1], (uint32_t)u & 1u);  // softmax B wrote P_B(u), keys 0-63
         TR(3, u);
         tc_fence_after();
-        issue_pv(1, u);
+        issue_pv(1, u, 0);
+        mbar_wait(&bars.p_full[1], (uint32_t)u & 1u);
+        tc_fence_after();
+        issue_pv(1, u, 1);
         mma_commit(&bars.empty[(2 * u + 1) % NSLOT]);  // V_u: both readers issued
         if (next) {
           issue_s(1, u + 1);
@@ -347,6 +355,15 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     auto give_token = [&]() {
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.tok[x ^ 1][qd]);
+    };
+    // P (bf16 pairs) over S in TMEM: half h = keys 64h..64h+63 -> columns 32h..32h+31
+    // (S of those columns is already in registers), then p_half / p_full
+    auto publish_half = [&](int hh) {
+      tmem_st_x32(trow + scol + 32 * hh, sr + 32 * hh);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(hh ? &bars.p_full[x] : &bars.p_half[x]);
     };
     for (int u = 0; u < cnt; ++u) {
       const int gk = walk.next();
@@ -400,20 +417,24 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
-          uint64_t p2;
-          if ((i & 7) < kEmu) {
-            p2 = exp2_poly2(x2);
-          } else {
-            float x0, x1;
-            unf2(x2, x0, x1);
-            p2 = f2(ex2(x0), ex2(x1));
+        for (int h2 = 0; h2 < 2; ++h2) {  // keys 0-63, then 64-127; P of the first half goes out early
+#pragma unroll
+          for (int i = 32 * h2; i < 32 * h2 + 32; ++i) {
+            const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
+            uint64_t p2;
+            if ((i & 7) < kEmu) {
+              p2 = exp2_poly2(x2);
+            } else {
+              float x0, x1;
+              unf2(x2, x0, x1);
+              p2 = f2(ex2(x0), ex2(x1));
+            }
+            acc2[i & 3] = fadd2(acc2[i & 3], p2);
+            float p0, p1;
+            unf2(p2, p0, p1);
+            sr[i] = pack_bf16(p0, p1);
           }
-          acc2[i & 3] = fadd2(acc2[i & 3], p2);
-          float p0, p1;
-          unf2(p2, p0, p1);
-          sr[i] = pack_bf16(p0, p1);
+          if (h2 == 0) publish_half(0);
         }
         const uint64_t t2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
         float a0, a1;
@@ -425,13 +446,10 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         if (kStagger) { take_token(u); give_token(); }
 #pragma unroll
         for (int i = 0; i < 64; ++i) sr[i] = 0u;  // block not selected by these rows: P = 0
+        publish_half(0);
       }
-      tmem_st_x32(trow + scol, sr);
-      tmem_st_x32(trow + scol + 32, sr + 32);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars.p_full[x]);
+      if (kMode == 1) publish_half(0);
+      publish_half(1);
       if (trx) TR(7 + 4 * x, u);
     }
     if (cnt > 0) {
@@ -497,6 +515,17 @@ cudaError_t launch_mode(const AttnArgs &a, const CUtensorMap &mq, const CUtensor
 }  // namespace pp
 }  // namespace sm100
 
+// BA_EXP_EMU (0..5; the gather paths support 0..2 and use 1 otherwise), read once
+static int emu_choice() {
+  static int emu = -1;
+  if (emu < 0) {
+    const char *e = getenv("BA_EXP_EMU");
+    emu = e ? atoi(e) : sm100::pp::kDefaultEmu;
+    if (emu < 0 || emu > 5) emu = sm100::pp::kDefaultEmu;
+  }
+  return emu;
+}
+
 bool attn_pp_supported(const AttnArgs &a) {
   return a.dtype == 0 && a.d == 128 && a.B == 128 && a.nk <= 32 * sm100::pp::kMaskWords;
 }
@@ -513,23 +542,33 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
                          : make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) && make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128));
     if (!ok) return cudaErrorInvalidValue;
     dim3 grid((unsigned)((a.nq + 1) / 2), (unsigned)(a.batch * a.hq));
-    if (gq && gkv) return launch_mode<0, kDefaultEmu, false, 3>(a, mq, mk, mv, grid, st);
-    if (gkv) return launch_mode<0, kDefaultEmu, false, 2>(a, mq, mk, mv, grid, st);
-    return launch_mode<0, kDefaultEmu, false, 1>(a, mq, mk, mv, grid, st);
+    // the copy path's exp2-offload variant (0..2), so both paths are bit-identical
+    const int e = emu_choice();
+    if (gq && gkv) {
+      if (e == 0) return launch_mode<0, 0, false, 3>(a, mq, mk, mv, grid, st);
+      if (e == 2) return launch_mode<0, 2, false, 3>(a, mq, mk, mv, grid, st);
+      return launch_mode<0, 1, false, 3>(a, mq, mk, mv, grid, st);
+    }
+    if (gkv) {
+      if (e == 0) return launch_mode<0, 0, false, 2>(a, mq, mk, mv, grid, st);
+      if (e == 2) return launch_mode<0, 2, false, 2>(a, mq, mk, mv, grid, st);
+      return launch_mode<0, 1, false, 2>(a, mq, mk, mv, grid, st);
+    }
+    if (e == 0) return launch_mode<0, 0, false, 1>(a, mq, mk, mv, grid, st);
+    if (e == 2) return launch_mode<0, 2, false, 1>(a, mq, mk, mv, grid, st);
+    return launch_mode<0, 1, false, 1>(a, mq, mk, mv, grid, st);
   }
   if (!make_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs, 128) || !make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) ||
       !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128))
     return cudaErrorInvalidValue;
-  static int dbg = -1, emu = -1, stagger = 0;
+  static int dbg = -1, stagger = 0;
+  const int emu = emu_choice();
   if (dbg < 0) {
     const char *sg = getenv("BA_PP_STAGGER");
     stagger = sg ? atoi(sg) : 0;  // measured slower (a lone warp cannot issue MUFU back to back): opt-in
     const char *d = getenv("BA_ATTN_DEBUG");
     dbg = d ? atoi(d) : 0;
     if (dbg < 0 || dbg > 2) dbg = 0;
-    const char *e = getenv("BA_EXP_EMU");
-    emu = e ? atoi(e) : kDefaultEmu;
-    if (emu < 0 || emu > 5) emu = kDefaultEmu;
   }
   dim3 grid((unsigned)((a.nq + 1) / 2), (unsigned)(a.batch * a.hq));
   if (dbg == 1) return launch_mode<1, 0>(a, mq, mk, mv, grid, st);
