@@ -32,18 +32,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, debug: bool = False, verbose: bool = True) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, debug: bool = False, verbose: bool = True, extra_flags=None, out: str = None) -> str:
+    """extra_flags / out: A/B builds (e.g. -DBA_PP_PSPLIT=4 into another .so, loaded via BA_LIB_PATH)."""
+    lib = out or LIB
+    if not force and not needs_build() and out is None:
         return LIB
     objs = []
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                     "-I", os.path.join(ROOT, "include"), "-Xptxas", "-v" if verbose and debug else "-O3"]
     if debug:
         flags += ["-DBA_DEBUG=1"]
+    flags += list(extra_flags or [])
     t0 = time.time()
     procs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        obj = os.path.join(CSRC, src.replace(".cu", ".o" if out is None else "_ab.o"))
         objs.append(obj)
         cmd = [nvcc()] + flags + ["-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
@@ -54,7 +57,7 @@ def build(force: bool = False, debug: bool = False, verbose: bool = True) -> str
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose and out.strip():
             sys.stderr.write(out)
-    cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcuda" if False else "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+    cmd = [nvcc()] + ARCH + ["-shared", "-o", lib] + objs + ["-lcuda" if False else "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -62,8 +65,8 @@ def build(force: bool = False, debug: bool = False, verbose: bool = True) -> str
     for o in objs:
         os.remove(o)
     if verbose:
-        print(f"built {LIB} in {time.time() - t0:.1f}s")
-    return LIB
+        print(f"built {lib} in {time.time() - t0:.1f}s")
+    return lib
 
 
 if __name__ == "__main__":

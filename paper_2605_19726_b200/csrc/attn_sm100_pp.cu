@@ -59,6 +59,10 @@ constexpr int NSLOT = 5;
 BA_DEVICE constexpr uint32_t s_col(int x) { return x ? 128u : 0u; }
 constexpr uint32_t O_COL0 = 256;
 constexpr int kProducerWarp = 8, kMmaWarp = 9;
+#ifndef BA_PP_PSPLIT
+#define BA_PP_PSPLIT 2
+#endif
+constexpr int kPSplit = BA_PP_PSPLIT;     // P handed to the MMA in this many key parts (2: +5% over 1; 4: -2% vs 2)
 constexpr int kThreads = 384;             // 12 warps: 8 softmax (warpgroups 0, 1) + warpgroup 2 (producer, MMA, 2 idle)
 constexpr int kRegsSoftmax = 208, kRegsSide = 80;  // setmaxnreg: 8*32*208 + 4*32*80 = 63488 <= 65536
 constexpr float kRescaleThreshold = 8.0f;
@@ -79,7 +83,7 @@ constexpr uint32_t IDESC_O = IDESC_S | (1u << 16);  // B = V MN-major (N = d = 1
 struct __align__(8) Bars {
   uint64_t q_full;
   uint64_t full[NSLOT], empty[NSLOT];
-  uint64_t s_full[2], p_half[2], p_full[2];  // per query block (A, B); p_half: P keys 0-63 in TMEM
+  uint64_t s_full[2], p_part[2][kPSplit];    // per query block (A, B); p_part[q]: P of key part q in TMEM
   uint64_t tok[2][4];             // MUFU token per SMSP: softmax A(u) -> B(u) -> A(u+1) ...
   uint64_t o_final;
   uint32_t tmem_base;
@@ -167,7 +171,10 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       bars.last_ragged = sel_last && (a.lk - gl * (int64_t)BN) < BN;
       mbar_init(&bars.q_full, 1);
       for (int s = 0; s < NSLOT; ++s) { mbar_init(&bars.full[s], 1); mbar_init(&bars.empty[s], 1); }
-      for (int s = 0; s < 2; ++s) { mbar_init(&bars.s_full[s], 1); mbar_init(&bars.p_half[s], 4); mbar_init(&bars.p_full[s], 4); }
+      for (int s = 0; s < 2; ++s) {
+        mbar_init(&bars.s_full[s], 1);
+        for (int q = 0; q < kPSplit; ++q) mbar_init(&bars.p_part[s][q], 4);
+      }
       for (int s = 0; s < 8; ++s) mbar_init(&bars.tok[s >> 2][s & 3], 1);
       mbar_init(&bars.o_final, 1);
       fence_barrier_init();
@@ -286,8 +293,9 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       // as soon as the softmax has stored P for keys 0-63 (p_half), overlapping its second half
       auto issue_pv = [&](int x, int u, int h) {
         const uint32_t sv = slot_addr(2 * u + 1);
+        constexpr int KPP = BN / 16 / kPSplit;  // 16-key MMA steps per part
 #pragma unroll
-        for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
+        for (int kk = KPP * h; kk < KPP * h + KPP; ++kk)
           mma_ts(tmem + O_COL0 + 128 * x, tmem + s_col(x) + kk * 8, make_desc(sv + kk * 2048, BOX, 1024), IDESC_O,
                  (u > 0 || kk > 0) ? 1u : 0u);
       };
@@ -297,25 +305,28 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       mma_commit(&bars.empty[0]);  // K_0 read by both
       for (int u = 0; u < cnt; ++u) {
         const bool next = u + 1 < cnt;
-        mbar_wait(&bars.p_half[0], (uint32_t)u & 1u);  // softmax A wrote P_A(u), keys 0-63
+        mbar_wait(&bars.p_part[0][0], (uint32_t)u & 1u);  // softmax A wrote P_A(u), first key part
         TR(1, u);
         wait_full(2 * u + 1);
         issue_pv(0, u, 0);
-        mbar_wait(&bars.p_full[0], (uint32_t)u & 1u);  // ... and keys 64-127
-        tc_fence_after();
-        issue_pv(0, u, 1);
+#pragma unroll
+        for (int q = 1; q < kPSplit; ++q) {
+          mbar_wait(&bars.p_part[0][q], (uint32_t)u & 1u);
+          tc_fence_after();
+          issue_pv(0, u, q);
+        }
         if (next) {
           wait_full(2 * u + 2);
           issue_s(0, u + 1);  // S_A buffer reuse: after PV_A(u) in issue order
           TR(2, u + 1);
         }
-        mbar_wait(&bars.p_half[1], (uint32_t)u & 1u);  // softmax B wrote P_B(u), keys 0-63
-        TR(3, u);
-        tc_fence_after();
-        issue_pv(1, u, 0);
-        mbar_wait(&bars.p_full[1], (uint32_t)u & 1u);
-        tc_fence_after();
-        issue_pv(1, u, 1);
+#pragma unroll
+        for (int q = 0; q < kPSplit; ++q) {
+          mbar_wait(&bars.p_part[1][q], (uint32_t)u & 1u);  // softmax B wrote P_B(u), key part q
+          if (q == 0) TR(3, u);
+          tc_fence_after();
+          issue_pv(1, u, q);
+        }
         mma_commit(&bars.empty[(2 * u + 1) % NSLOT]);  // V_u: both readers issued
         if (next) {
           issue_s(1, u + 1);
@@ -356,14 +367,16 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.tok[x ^ 1][qd]);
     };
-    // P (bf16 pairs) over S in TMEM: half h = keys 64h..64h+63 -> columns 32h..32h+31
-    // (S of those columns is already in registers), then p_half / p_full
-    auto publish_half = [&](int hh) {
-      tmem_st_x32(trow + scol + 32 * hh, sr + 32 * hh);
+    // P (bf16 pairs) over S in TMEM: part q = keys 128q/kPSplit .. -> columns 64q/kPSplit ..
+    // (S of those columns is already in registers), then p_part[q]
+    auto publish_part = [&](int q) {
+      constexpr int W = 64 / kPSplit;  // TMEM columns per part
+      if constexpr (W == 32) tmem_st_x32(trow + scol + W * q, sr + W * q);
+      else tmem_st_x16(trow + scol + W * q, sr + W * q);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(hh ? &bars.p_full[x] : &bars.p_half[x]);
+      if (lane == 0) mbar_arrive(&bars.p_part[x][q]);
     };
     for (int u = 0; u < cnt; ++u) {
       const int gk = walk.next();
@@ -417,9 +430,10 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {  // keys 0-63, then 64-127; P of the first half goes out early
+        for (int h2 = 0; h2 < kPSplit; ++h2) {  // key parts in order; each part's P goes out as soon as done
+          constexpr int PP = 64 / kPSplit;       // packed pairs per part
 #pragma unroll
-          for (int i = 32 * h2; i < 32 * h2 + 32; ++i) {
+          for (int i = PP * h2; i < PP * h2 + PP; ++i) {
             const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
             uint64_t p2;
             if ((i & 7) < kEmu) {
@@ -434,7 +448,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
             unf2(p2, p0, p1);
             sr[i] = pack_bf16(p0, p1);
           }
-          if (h2 == 0) publish_half(0);
+          if (h2 < kPSplit - 1) publish_part(h2);
         }
         const uint64_t t2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
         float a0, a1;
@@ -446,10 +460,14 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         if (kStagger) { take_token(u); give_token(); }
 #pragma unroll
         for (int i = 0; i < 64; ++i) sr[i] = 0u;  // block not selected by these rows: P = 0
-        publish_half(0);
+#pragma unroll
+        for (int q = 0; q < kPSplit - 1; ++q) publish_part(q);
       }
-      if (kMode == 1) publish_half(0);
-      publish_half(1);
+      if (kMode == 1) {
+#pragma unroll
+        for (int q = 0; q < kPSplit - 1; ++q) publish_part(q);
+      }
+      publish_part(kPSplit - 1);
       if (trx) TR(7 + 4 * x, u);
     }
     if (cnt > 0) {
