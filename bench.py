@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / e2e / cpu legs)")
+    ap.add_argument("--fused", action="store_true",
+                    help="with --shard heads: fuse the output all-gather into the attention epilogue (peer stores "
+                         "into symmetric memory, ba_sparse_attn_peers) instead of an NCCL all-gather")
     ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
                     help="batch: weak scaling, rank r runs its own batch element (default); heads: strong "
                          "scaling, rank r runs a slice of whole GQA groups and O is all-gathered (NCCL)")
@@ -231,12 +234,13 @@ def run_ours(args):
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or (args.fused and "MASTER_ADDR" in os.environ):  # symmetric memory needs a process group
         dist.init_process_group("nccl", device_id=dev)
     ba.load()
     w = CONFIGS[args.config]
     density = args.density if args.density is not None else w.density
-    heads = args.shard == "heads" and world > 1
+    heads = args.shard == "heads" and (world > 1 or args.fused)
+    fused = None
     if heads:
         # strong scaling: every rank builds the same problem and keeps whole GQA groups
         q, k, v = make_qkv(w, device=dev)
@@ -251,18 +255,34 @@ def run_ours(args):
     # (no copies), --q-in-place only Q read through pi_q
     zero_copy = (True if args.zero_copy and ba.zero_copy_supported(q, k, v, w.block_size)
                  else "q" if args.q_in_place and ba.q_gather_supported(q, k, v, w.block_size) else False)
-    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", args.comp, top_p=args.top_p, zero_copy=zero_copy)
-    out = torch.empty_like(q)
+    if heads and args.fused:
+        # the output collective fused into the attention epilogue: full O in symmetric memory on
+        # every rank, each rank's kernel stores its heads' rows into all copies (NVLink peer stores)
+        from paper_2605_19726_b200.dist import FusedHeadGather
+        fused = FusedHeadGather((q.shape[0], w.heads_q, q.shape[2], q.shape[3]), q.dtype, dev, q0)
+        out = fused.full[:, q0:q1]
+    else:
+        out = torch.empty_like(q)
+    ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", args.comp, top_p=args.top_p, zero_copy=zero_copy,
+                     out=out)
     stream = torch.cuda.current_stream()
+
+    def attn_and_gather():
+        if fused is not None:
+            ctx.sparse_attn_peers(fused.peer_ptrs)
+            n = ba.last_launch_count()
+            fused.barrier()
+            return n
+        ctx.sparse_attn(out)
+        n = ba.last_launch_count()
+        if heads:
+            gather_heads(out, w.heads_q)  # the path's only collective (NCCL all-gather over NVLink)
+        return n
 
     def step():
         ctx.select(q, k, v)
         n_sel = ba.last_launch_count()
-        ctx.sparse_attn(out)
-        n = n_sel + ba.last_launch_count()
-        if heads:
-            gather_heads(out, w.heads_q)  # the path's only collective (NCCL all-gather over NVLink)
-        return n
+        return n_sel + attn_and_gather()
 
     for _ in range(max(args.warmup, 1)):
         launches = step()
@@ -285,10 +305,15 @@ def run_ours(args):
         ev[i][0].record(stream)
         ctx.select(q, k, v)
         ev[i][1].record(stream)
-        ctx.sparse_attn(out)
-        ev[i][2].record(stream)
-        if heads:
-            gather_heads(out, w.heads_q)
+        if fused is not None:
+            ctx.sparse_attn_peers(fused.peer_ptrs)
+            ev[i][2].record(stream)
+            fused.barrier()
+        else:
+            ctx.sparse_attn(out)
+            ev[i][2].record(stream)
+            if heads:
+                gather_heads(out, w.heads_q)
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -419,7 +444,9 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": workload_desc(w, density, args.top_p, args.comp), "global_batch": 1 if heads else world,
                        "seq_len": w.seq_len,
-                       "parallelism": (f"head-parallel x{world} (whole GQA groups per rank, NCCL all-gather of O)"
+                       "parallelism": (f"head-parallel x{world} (whole GQA groups per rank, "
+                                       + ("O gathered by peer stores in the attention epilogue)" if fused is not None
+                                          else "NCCL all-gather of O)")
                                        if heads else f"batch-parallel x{world} (weak scaling, no data-path collective)"),
                        "l2": "inputs larger than L2 (q+k+v = %.2f GB per step)" %
                              ((q.numel() + k.numel() + v.numel()) * 2 / 1e9),
@@ -443,7 +470,7 @@ def run_ours(args):
             line["fidelity"] = fidelity
         line.update(res)
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

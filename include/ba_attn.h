@@ -203,6 +203,21 @@ ba_status ba_sparse_attn_gather(const ba_problem *prob, const ba_params *params,
  * needed), 0 = neither (use ba_sparse_attn).  No device work. */
 int ba_zero_copy_supported(const ba_problem *prob, const ba_params *params);
 
+/* Alg. 1 steps 11-12 with the head-parallel output collective fused into the
+ * epilogue: every output row is stored to EACH of the
+ * n_peers buffers out_peers[0..n_peers) (device pointers valid in this
+ * process — e.g. the peers' symmetric-memory buffers mapped over NVLink /
+ * NVSwitch, each pre-offset to this rank's head slice; same o_stride layout),
+ * so after a barrier every rank holds the whole O without an all-gather pass.
+ * Otherwise as ba_sparse_attn (reads the permuted copies).  1 <= n_peers <= 8;
+ * bf16, head_dim 128 (the tcgen05 pair / single-CTA kernels), else
+ * BA_ERR_UNSUPPORTED.  The library performs no cross-rank synchronisation: the
+ * caller orders the peers' reads after every rank's kernel (e.g. a symmetric
+ * memory barrier). */
+ba_status ba_sparse_attn_peers(const ba_problem *prob, const ba_params *params,
+                               const ba_selection *sel, void *const *out_peers, int n_peers,
+                               float *lse, cudaStream_t stream);
+
 /* ba_select + attention with the selection carved from the workspace
  * (>= ba_attention_workspace_size bytes), on the permuted copies
  * (ba_sparse_attn) — the faster path on B200.  The environment

@@ -86,6 +86,8 @@ def load() -> ctypes.CDLL:
     lib.ba_block_mass_workspace_size.restype = sz
     lib.ba_block_mass.argtypes = [P, PA, S, vp, vp, vp, sz, st]
     lib.ba_block_mass.restype = ctypes.c_int
+    lib.ba_sparse_attn_peers.argtypes = [P, PA, S, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, vp, st]
+    lib.ba_sparse_attn_peers.restype = ctypes.c_int
     lib.ba_zero_copy_supported.argtypes = [P, PA]
     lib.ba_zero_copy_supported.restype = ctypes.c_int
     lib.ba_attention.argtypes = [P, PA, vp, vp, vp, vp, vp, vp, sz, st]
@@ -105,7 +107,7 @@ def load() -> ctypes.CDLL:
 
 
 EXPORTED = ["ba_abi_version", "ba_selection_sizes", "ba_select_workspace_size", "ba_attention_workspace_size",
-            "ba_select", "ba_sparse_attn", "ba_sparse_attn_gather", "ba_zero_copy_supported",
+            "ba_select", "ba_sparse_attn", "ba_sparse_attn_gather", "ba_sparse_attn_peers", "ba_zero_copy_supported",
             "ba_attention", "ba_dense_attn", "ba_block_mass_workspace_size", "ba_block_mass",
             "ba_attention_host_workspace_size", "ba_attention_host", "ba_last_launch_count",
             "ba_attention_kernel_name",
@@ -300,6 +302,14 @@ class Context:
         _check(lib.ba_block_mass(ctypes.byref(self.prob), ctypes.byref(self.params), ctypes.byref(self.sel_c),
                                  _ptr(m_hat), _ptr(cap), _ptr(ws), ws.numel(), _stream(stream)))
         return m_hat, cap
+
+    def sparse_attn_peers(self, peer_ptrs, lse=None, stream=None):
+        """Fused output collective: store every output row to each of the device
+        pointers in peer_ptrs (ba_sparse_attn_peers); strides are those of `out`
+        given at construction (contiguous [b, Hq, Lq, d] by default)."""
+        arr = (ctypes.c_void_p * len(peer_ptrs))(*[ctypes.c_void_p(int(p)) for p in peer_ptrs])
+        _check(load().ba_sparse_attn_peers(ctypes.byref(self.prob), ctypes.byref(self.params), ctypes.byref(self.sel_c),
+                                           arr, len(peer_ptrs), _ptr(lse), _stream(stream)))
 
     def sparse_attn(self, out, lse=None, sel: Optional[Selection] = None, stream=None):
         sc = self.sel_c if sel is None else sel.to_c()

@@ -486,6 +486,37 @@ int ba_zero_copy_supported(const ba_problem *prob, const ba_params *params) {
   return gather_unsupported(D, prob, false) == nullptr ? 1 : 0;
 }
 
+ba_status ba_sparse_attn_peers(const ba_problem *prob, const ba_params *params, const ba_selection *sel,
+                               void *const *out_peers, int n_peers, float *lse, cudaStream_t stream) {
+  g_err.clear();
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  if (!out_peers || n_peers < 1 || n_peers > kMaxPeers)
+    return fail(BA_ERR_INVALID_ARGUMENT, "n_peers = %d (1..%d) / out_peers NULL", n_peers, kMaxPeers);
+  for (int p = 0; p < n_peers; ++p) {
+    char name[32];
+    snprintf(name, sizeof(name), "out_peers[%d]", p);
+    BA_TRY(check_ptr(name, out_peers[p]));
+  }
+  if (!sel || !sel->q_sorted || !sel->k_sorted || !sel->v_sorted || !sel->kv_index || !sel->kv_count || !sel->perm_q)
+    return fail(BA_ERR_INVALID_ARGUMENT, "ba_sparse_attn_peers reads the permuted copies, kv_index, kv_count, perm_q");
+  BA_TRY(check_strides("o", prob->o_stride, D.esz));
+  AttnArgs a = make_attn(D, params);
+  if (!attn_sm100_supported(a) || use_pps(a) || use_2cta(a))
+    return fail(BA_ERR_UNSUPPORTED, "peer stores need the bf16 tcgen05 pair / single-CTA kernels (d = 128)");
+  a.q = sel->q_sorted; a.k = sel->k_sorted; a.v = sel->v_sorted;
+  a.qs[0] = D.hq * D.lq * D.d; a.qs[1] = D.lq * D.d; a.qs[2] = D.d;
+  a.ks[0] = D.hkv * D.lk * D.d; a.ks[1] = D.lk * D.d; a.ks[2] = D.d;
+  for (int i = 0; i < 3; ++i) a.vs[i] = a.ks[i];
+  a.kv_index = sel->kv_index; a.kv_count = sel->kv_count; a.kv_stride = D.kappa; a.perm_q = sel->perm_q;
+  a.out = out_peers[0];
+  a.n_peers = n_peers;
+  for (int p = 0; p < n_peers; ++p) a.out_peers[p] = out_peers[p];
+  for (int i = 0; i < 3; ++i) a.os[i] = prob->o_stride[i];
+  a.lse = lse;
+  return run_attn(a, stream);
+}
+
 ba_status ba_attention(const ba_problem *prob, const ba_params *params, const void *q, const void *k,
                        const void *v, void *out, float *lse, void *workspace, size_t workspace_bytes,
                        cudaStream_t stream) {

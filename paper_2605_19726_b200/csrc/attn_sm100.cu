@@ -485,7 +485,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
     const float inv = lt > 0.f ? 1.f / lt : 0.f;
     int64_t orow = row0 + r;
     if (r < nrows && a.perm_q) orow = a.perm_q[bh * a.lq + row0 + r];
-    __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(a.out) + b * a.os[0] + h * a.os[1] + orow * a.os[2] + hf * 64;
+    const int64_t o_off = b * a.os[0] + h * a.os[1] + orow * a.os[2] + hf * 64;
 #pragma unroll
     for (int q2 = 0; q2 < 2; ++q2) {
       uint32_t ov[32];
@@ -496,9 +496,9 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       for (int i = 0; i < 16; ++i)
         pk[i] = pack_bf16(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
       if (r < nrows) {
-        uint4 *dst = reinterpret_cast<uint4 *>(o + q2 * 32);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int i = 0; i < 4; ++i)
+          store_out_row16<__nv_bfloat16>(a, o_off + q2 * 32 + 8 * i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
       }
     }
     if (a.lse && hf == 0 && r < nrows) a.lse[bh * a.lq + orow] = lt > 0.f ? (m + log2f(lt)) * 0.69314718055994531f : -INFINITY;

@@ -477,7 +477,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     const float inv = l > 0.f ? 1.f / l : 0.f;
     int64_t orow = row0 + r;
     if (r < nrows && a.perm_q) orow = a.perm_q[bh * a.lq + row0 + r];
-    __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(a.out) + b * a.os[0] + h * a.os[1] + orow * a.os[2];
+    const int64_t o_off = b * a.os[0] + h * a.os[1] + orow * a.os[2];
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
       uint32_t ov[32];
@@ -487,9 +487,9 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
 #pragma unroll
       for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
       if (r < nrows) {
-        uint4 *dst = reinterpret_cast<uint4 *>(o + q4 * 32);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int i = 0; i < 4; ++i)
+          store_out_row16<__nv_bfloat16>(a, o_off + q4 * 32 + 8 * i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
       }
     }
     if (a.lse && r < nrows) a.lse[bh * a.lq + orow] = l > 0.f ? (m + log2f(l)) * 0.69314718055994531f : -INFINITY;

@@ -60,6 +60,7 @@ cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, double top_p, c
                         double *tau, cudaStream_t st);
 
 // ---------------------------------------------------------------- attention
+constexpr int kMaxPeers = 8;
 struct AttnArgs {
   int dtype;          // 0 bf16, 1 fp32
   int d;              // head dim
@@ -81,6 +82,11 @@ struct AttnArgs {
   // tile::gather4 (4 rows per instruction) instead of reading permuted copies
   int gather;
   const int32_t *perm_k;       // [b, hkv, lk] (gather only)
+  // fused output collective (head-parallel all-gather over NVLink peer memory): when
+  // n_peers > 0 every output row is stored to each out_peers[p] (same offsets / strides
+  // as out) instead of out — the peers' symmetric buffers, pre-offset to this rank's heads
+  int n_peers;
+  void *out_peers[kMaxPeers];
 };
 cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t st);
 cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st);

@@ -6,7 +6,21 @@
 
 #include "common.cuh"
 
+#include "kernels.h"
+
 namespace baatt {
+
+// Store one 16-byte vector of an output row to `out` (n_peers == 0) or to every peer
+// buffer at the same element offset (the fused head-parallel all-gather).
+template <typename T>
+BA_DEVICE void store_out_row16(const AttnArgs &a, int64_t elem_off, uint4 v) {
+  if (a.n_peers == 0) {
+    *reinterpret_cast<uint4 *>(static_cast<T *>(a.out) + elem_off) = v;
+  } else {
+    for (int p = 0; p < a.n_peers; ++p) *reinterpret_cast<uint4 *>(static_cast<T *>(a.out_peers[p]) + elem_off) = v;
+  }
+}
+
 namespace sm100 {
 
 // ------------------------------------------------------------------ PTX wrappers

@@ -71,3 +71,31 @@ def sum_over_ranks(x: float, device) -> float:
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def peer_slice_ptrs(buffer_ptrs, q0: int, head_stride_elems: int, elem_size: int):
+    """Device pointers of every rank's full-O buffer advanced to this rank's first
+    head q0 — the out_peers of ba_sparse_attn_peers (its kernel adds the local
+    head / token offsets with the full buffer's strides)."""
+    off = q0 * head_stride_elems * elem_size
+    return [int(p) + off for p in buffer_ptrs]
+
+
+class FusedHeadGather:
+    """Head-parallel output reassembly fused into the attention epilogue: the
+    full O [b, Hq, L, d] lives in symmetric memory on every rank, and each
+    rank's kernel stores its heads' rows into all ranks' copies over NVLink /
+    NVSwitch (ba_sparse_attn_peers); a symmetric-memory barrier then orders the
+    reads.  Replaces the NCCL all-gather of gather_heads."""
+
+    def __init__(self, shape_full, dtype, device, q0: int, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        if not dist.is_initialized():
+            raise RuntimeError("FusedHeadGather needs an initialised process group (launch under torchrun)")
+        group = group or dist.group.WORLD
+        self.full = symm_mem.empty(*shape_full, dtype=dtype, device=device)
+        self.handle = symm_mem.rendezvous(self.full, group)
+        self.peer_ptrs = peer_slice_ptrs(self.handle.buffer_ptrs, q0, self.full.stride(1), self.full.element_size())
+
+    def barrier(self):
+        self.handle.barrier()

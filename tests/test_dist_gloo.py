@@ -69,3 +69,20 @@ def test_gather_heads_world2(hq, hkv):
         p.join(timeout=60)
     assert all(ok for _, ok, _, _ in res), res
     assert all(mx == 2.0 and sm == 3.0 for _, _, mx, sm in res), res
+
+
+def test_peer_slice_ptrs():
+    """out_peers of the fused head-parallel epilogue: every rank's buffer base
+    advanced by q0 heads of the full buffer (element strides x element size)."""
+    from paper_2605_19726_b200.dist import peer_slice_ptrs
+    b, hq, L, d = 2, 32, 1000, 128
+    full = torch.empty(b, hq, L, d, dtype=torch.bfloat16)
+    for world in (1, 2, 4, 8):
+        bases = [0x10000000 * (r + 1) for r in range(world)]
+        for rank in range(world):
+            q0, q1, _, _ = head_range(hq, 8, world, rank)
+            ptrs = peer_slice_ptrs(bases, q0, full.stride(1), full.element_size())
+            assert ptrs == [bb + q0 * L * d * 2 for bb in bases]
+            # the local head h of this rank lands on global head q0 + h of every copy
+            h = q1 - q0 - 1
+            assert ptrs[0] + h * full.stride(1) * 2 == bases[0] + (q0 + h) * L * d * 2

@@ -455,3 +455,28 @@ def test_block_mass_fullsize_properties(ba):
     c = cap[0, 0].double()
     assert (c <= greedy + 1e-4).all()
     assert c.mean() > kap / sel.n_k + 0.05
+
+
+# ---------------------------------------------------------------- fused output collective (peer stores)
+@pytest.mark.parametrize("cfg,L,hq,hkv,B", [("C", 2048 + 64, 4, 1, 128), ("M", 2048 + 33, 2, 2, 64)])
+def test_sparse_attn_peers_broadcast(ba, cfg, L, hq, hkv, B):
+    """ba_sparse_attn_peers stores every output row to each peer buffer (here
+    three buffers of one device, slices of a larger 'full' buffer as a
+    head-parallel rank would see them): each copy equals ba_sparse_attn."""
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv)
+    ref = torch.empty_like(q)
+    ctx0 = ba.Context(q, k, v, B, 0.5)
+    ctx0.select(q, k, v)
+    ctx0.sparse_attn(ref)
+    # full buffers of 2*hq heads; this "rank" owns heads [hq, 2*hq)
+    fulls = [torch.full((1, 2 * hq, L, 128), float("nan"), dtype=q.dtype, device="cuda") for _ in range(3)]
+    from paper_2605_19726_b200.dist import peer_slice_ptrs
+    ptrs = peer_slice_ptrs([f.data_ptr() for f in fulls], hq, fulls[0].stride(1), 2)
+    ctx = ba.Context(q, k, v, B, 0.5, out=fulls[0][:, hq:])
+    ctx.select(q, k, v)
+    ctx.sparse_attn_peers(ptrs)
+    torch.cuda.synchronize()
+    for f in fulls:
+        assert torch.equal(f[:, hq:], ref)
+        assert torch.isnan(f[:, :hq].float()).all()  # nothing written outside this rank's heads
