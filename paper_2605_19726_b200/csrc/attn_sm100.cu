@@ -88,7 +88,7 @@ template <int NKV>
 struct __align__(8) BarsT {
   uint64_t q_full;
   uint64_t kv_full[NKV], kv_empty[NKV];
-  uint64_t s_full[2], p_full[2];
+  uint64_t s_full[2], p_q[2][2][2];  // p_q[buf][column half][part]: that part's P is in TMEM (4 warps)
   uint64_t o_done;
   uint64_t o_final;  // single phase: every PV of the tile has completed (epilogue)
   uint32_t tmem_base;
@@ -195,7 +195,10 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
   if (warp == 0 && lane == 0) {
     mbar_init(&bars.q_full, 8);   // one elected arrive per softmax warp
     for (int s = 0; s < C::NKV; ++s) { mbar_init(&bars.kv_full[s], 1); mbar_init(&bars.kv_empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&bars.s_full[s], 1); mbar_init(&bars.p_full[s], 8); }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars.s_full[s], 1);
+      for (int q = 0; q < 4; ++q) mbar_init(&bars.p_q[s][q >> 1][q & 1], 4);
+    }
     mbar_init(&bars.o_done, 1);
     mbar_init(&bars.o_final, 1);
     fence_barrier_init();
@@ -303,17 +306,25 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       issue_s(0);
       for (int j = 0; j < cnt; ++j) {
         if (j + 1 < cnt) issue_s(j + 1);
-        mbar_wait(&bars.p_full[j & 1], (uint32_t)(j >> 1) & 1u);
-        TR(3, j);
         const int s = j % C::NKV;  // V_j arrived with K_j (waited in issue_s(j))
-        TR(4, j);
-        tc_fence_after();
         const uint32_t sv = base + C::SMEM_KV + s * 2 * C::TILE_BYTES + C::TILE_BYTES;
+        // PV_j in four key parts, each issued as soon as its softmax warps stored that P part:
+        // (half 0, part 0), (half 1, part 0), (half 0, part 1), (half 1, part 1)
+        constexpr int KH = kBN / 32, KQ = KH / 2;  // 16-key steps per column half / per part
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          mma_ts(tmem + O_COL, tmem + C::s_col(j & 1) + kk * 8, make_desc(sv + kk * 2048, C::BOX_BYTES, 1024),
-                 C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int pq = 0; pq < 4; ++pq) {
+          const int hh = pq & 1, q = pq >> 1;
+          mbar_wait(&bars.p_q[j & 1][hh][q], (uint32_t)(j >> 1) & 1u);
+          if (pq == 0) TR(3, j);
+          tc_fence_after();
+#pragma unroll
+          for (int t2 = 0; t2 < KQ; ++t2) {
+            const int kk = hh * KH + q * KQ + t2;
+            mma_ts(tmem + O_COL, tmem + C::s_col(j & 1) + kk * 8, make_desc(sv + kk * 2048, C::BOX_BYTES, 1024),
+                   C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+          }
         }
+        TR(4, j);
         mma_commit(&bars.kv_empty[s]);  // stage free once PV_j (the last reader of K_j / V_j) completes
         mma_commit(&bars.o_done);
       }
@@ -379,7 +390,7 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       if constexpr (kNoSoftmax) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars.p_full[j & 1]);
+        if (lane == 0) { mbar_arrive(&bars.p_q[j & 1][hf][0]); mbar_arrive(&bars.p_q[j & 1][hf][1]); }
         continue;
       }
       if (mine) {
@@ -435,12 +446,23 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
           }
         }
       }
+      // P part q of this column half (packed pairs [q*HC/4, (q+1)*HC/4)) over S in TMEM, then signal
+      auto publish = [&](int q) {
+        constexpr int W = HC / 4;  // TMEM columns per part
+        if constexpr (W == 16) tmem_st_x16(trow + C::s_col(j & 1) + hf * (HC / 2) + q * W, sr + q * W);
+        else tmem_st_x8(trow + C::s_col(j & 1) + hf * (HC / 2) + q * W, sr + q * W);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();  // all 32 lanes' P stores are complete before the warp's single arrive
+        if (lane == 0) mbar_arrive(&bars.p_q[j & 1][hf][q]);
+      };
       if (mine) {
         // p = 2^(s*c - m): FFMA2 for the argument, MUFU or polynomial exp2, FADD2 row sums
         const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
         for (int i = 0; i < HC / 2; ++i) {
+          if (i == HC / 4) publish(0);  // the first part's P goes out while the second is exponentiated
           const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
           uint64_t p2;
           if ((i & 7) < kEmu) {
@@ -462,14 +484,10 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       } else {
 #pragma unroll
         for (int i = 0; i < HC / 2; ++i) sr[i] = 0u;  // block not selected by these rows: P = 0
+        publish(0);
       }
       if (lane == 0 && qd == 0) TR(8 + 5 * hf, j);
-      if constexpr (HC / 2 == 32) tmem_st_x32(trow + C::s_col(j & 1) + hf * (HC / 2), sr);
-      else tmem_st_x16(trow + C::s_col(j & 1) + hf * (HC / 2), sr);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();  // all 32 lanes' P stores are complete before the warp's single arrive
-      if (lane == 0) mbar_arrive(&bars.p_full[j & 1]);
+      publish(1);
       if (lane == 0 && qd == 0) TR(9 + 5 * hf, j);
     }
     // epilogue: l = sum of both halves; each half writes its 64 output columns
