@@ -241,17 +241,23 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   double *q_var = sel->q_var ? sel->q_var : at<double>(ws, plan.q_var);
   double *k_mean = sel->k_mean ? sel->k_mean : at<double>(ws, plan.k_mean);
   double *k_var = sel->k_var ? sel->k_var : at<double>(ws, plan.k_var);
-  BA_TRY(cuda_check(launch_gather_stats(D.dtype, (int)D.d, q, prob->q_stride, D.b, D.hq, D.lq, (int)D.B,
-                                        sort_q(pa) ? sel->perm_q : nullptr, sort_q(pa) ? nullptr : sel->perm_q,
-                                        sel->q_sorted, q_mean, q_var, st), "gather_stats(q)"));
-  BA_TRY(cuda_check(launch_gather_stats(D.dtype, (int)D.d, k, prob->k_stride, D.b, D.hkv, D.lk, (int)D.B,
-                                        sort_k(pa) ? sel->perm_k : nullptr, sort_k(pa) ? nullptr : sel->perm_k,
-                                        sel->k_sorted, k_mean, k_var, st), "gather_stats(k)"));
-  launches += 2;
-  if (sel->v_sorted) {
-    BA_TRY(cuda_check(launch_gather_stats(D.dtype, (int)D.d, v, prob->v_stride, D.b, D.hkv, D.lk, (int)D.B,
-                                          sort_k(pa) ? sel->perm_k : nullptr, nullptr, sel->v_sorted, nullptr,
-                                          nullptr, st), "gather(v)"));
+  {  // Q, K (+ V copy) in one launch
+    GatherSides gs;
+    auto side = [&](const void *x, const int64_t *stv, int64_t heads, int64_t L, const int32_t *perm,
+                    int32_t *perm_id_out, void *xs, double *mean, double *var) {
+      GatherSide &sd = gs.side[gs.n++];
+      sd.x = x;
+      for (int i = 0; i < 3; ++i) sd.st[i] = stv[i];
+      sd.batch = D.b; sd.heads = heads; sd.L = L; sd.perm = perm; sd.perm_id_out = perm_id_out;
+      sd.xs = xs; sd.mean = mean; sd.var = var;
+    };
+    side(q, prob->q_stride, D.hq, D.lq, sort_q(pa) ? sel->perm_q : nullptr, sort_q(pa) ? nullptr : sel->perm_q,
+         sel->q_sorted, q_mean, q_var);
+    side(k, prob->k_stride, D.hkv, D.lk, sort_k(pa) ? sel->perm_k : nullptr, sort_k(pa) ? nullptr : sel->perm_k,
+         sel->k_sorted, k_mean, k_var);
+    if (sel->v_sorted) side(v, prob->v_stride, D.hkv, D.lk, sort_k(pa) ? sel->perm_k : nullptr, nullptr, sel->v_sorted,
+                            nullptr, nullptr);
+    BA_TRY(cuda_check(launch_gather_stats_multi(D.dtype, (int)D.d, gs, (int)D.B, st), "gather_stats"));
     ++launches;
   }
   // K4: scores, then per-row top-kappa

@@ -50,6 +50,22 @@ cudaError_t launch_gather_stats(int dtype, int d, const void *x, const int64_t *
 cudaError_t launch_block_cov(int dtype, int d, const void *x, const int64_t *stride, int64_t batch, int64_t heads,
                              int64_t L, int B, const int32_t *perm, const double *mean, double *cov, cudaStream_t st);
 // comp: 0 none, 1 diagonal (q_var / k_var = variances), 2 exact (q_var / k_var = covariances)
+// K3 for several tensors (Q, K, V) in one launch
+struct GatherSide {
+  const void *x;
+  int64_t st[3];
+  int64_t batch, heads, L;
+  const int32_t *perm;      // nullptr = identity
+  int32_t *perm_id_out;     // identity permutation written here when perm == nullptr (or nullptr)
+  void *xs;                 // permuted copy or nullptr
+  double *mean, *var;       // nullptr = copy only
+  int64_t ctas;             // filled by the launcher
+};
+struct GatherSides {
+  GatherSide side[3];
+  int n = 0;
+};
+cudaError_t launch_gather_stats_multi(int dtype, int d, GatherSides gs, int B, cudaStream_t st);
 cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk,
                           const double *q_mean, const double *q_var, const double *k_mean,
                           const double *k_var, int comp, double beta, double *logits,

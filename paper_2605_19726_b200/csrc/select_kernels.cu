@@ -352,10 +352,10 @@ cudaError_t launch_radix_sort(const SortGeom &g, uint32_t *keys_a, uint32_t *val
 // eps * (var + (mean - K)^2) instead of eps * (var + mean^2).
 // =====================================================================================
 template <typename T, int D>
-__global__ void __launch_bounds__(256, 3) gather_stats_kernel(
-    const T *__restrict__ x, int64_t s0, int64_t s1, int64_t s2, int64_t heads, int64_t L, int B,
-    const int32_t *__restrict__ perm, int32_t *__restrict__ perm_id_out, T *__restrict__ xs,
-    double *__restrict__ mean, double *__restrict__ var) {
+BA_DEVICE void gather_stats_body(const T *__restrict__ x, int64_t s0, int64_t s1, int64_t s2, int64_t heads, int64_t L,
+                                 int B, const int32_t *__restrict__ perm, int32_t *__restrict__ perm_id_out,
+                                 T *__restrict__ xs, double *__restrict__ mean, double *__restrict__ var, int64_t g,
+                                 int64_t bh) {
   constexpr int EPC = Chunk<T>::EPC;
   constexpr int CPR = D / EPC;       // chunks per row
   constexpr int RPI = 256 / CPR;     // rows per iteration
@@ -365,9 +365,7 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
   constexpr int RG = RPI / GPW;                 // partial rows left for the smem reduction
   __shared__ double red[2][RG][D + 1];
   __shared__ double s_shift[D];
-  const int64_t g = blockIdx.x;
-  const int64_t bh = blockIdx.y;  // batch * heads + head
-  const int64_t b = bh / heads, h = bh - b * heads;
+  const int64_t b = bh / heads, h = bh - b * heads;  // g: block, bh: batch * heads + head
   const int chunk = threadIdx.x % CPR;
   const int rsub = threadIdx.x / CPR;
   const int64_t row0 = g * B;
@@ -452,6 +450,44 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
     mean[(bh * nb + g) * D + c] = s_shift[c] + m1;
     var[(bh * nb + g) * D + c] = fmax(fma(-m1, m1, t2 * inv_n), 0.0);
   }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256, 3) gather_stats_kernel(
+    const T *__restrict__ x, int64_t s0, int64_t s1, int64_t s2, int64_t heads, int64_t L, int B,
+    const int32_t *__restrict__ perm, int32_t *__restrict__ perm_id_out, T *__restrict__ xs,
+    double *__restrict__ mean, double *__restrict__ var) {
+  gather_stats_body<T, D>(x, s0, s1, s2, heads, L, B, perm, perm_id_out, xs, mean, var, blockIdx.x, blockIdx.y);
+}
+
+// Q, K and V of one ba_select in ONE launch (one CTA per (side, block, batch*head),
+// sides laid out back to back in a 1-D grid): no inter-kernel drain between them.
+template <typename T, int D>
+__global__ void __launch_bounds__(256, 3) gather_stats_multi_kernel(const GatherSides gs, int B) {
+  int64_t c = blockIdx.x;
+  int s = 0;
+  while (s + 1 < gs.n && c >= gs.side[s].ctas) { c -= gs.side[s].ctas; ++s; }
+  const GatherSide &sd = gs.side[s];
+  const int64_t nb = (sd.L + B - 1) / B;
+  gather_stats_body<T, D>(static_cast<const T *>(sd.x), sd.st[0], sd.st[1], sd.st[2], sd.heads, sd.L, B, sd.perm,
+                          sd.perm_id_out, static_cast<T *>(sd.xs), sd.mean, sd.var, c % nb, c / nb);
+}
+
+cudaError_t launch_gather_stats_multi(int dtype, int d, GatherSides gs, int B, cudaStream_t stream) {
+  int64_t total = 0;
+  for (int s = 0; s < gs.n; ++s) {
+    gs.side[s].ctas = ((gs.side[s].L + B - 1) / B) * gs.side[s].heads * gs.side[s].batch;
+    total += gs.side[s].ctas;
+  }
+  if (total == 0) return cudaSuccess;
+  // heads in gather_stats_body index one batch element's heads; bh runs over batch * heads
+#define BA_GM(T, D) gather_stats_multi_kernel<T, D><<<(unsigned)total, 256, 0, stream>>>(gs, B)
+  if (dtype == 0 && d == 128) BA_GM(__nv_bfloat16, 128);
+  else if (dtype == 0 && d == 64) BA_GM(__nv_bfloat16, 64);
+  else if (dtype == 1 && d == 128) BA_GM(float, 128);
+  else BA_GM(float, 64);
+#undef BA_GM
+  return cudaGetLastError();
 }
 
 cudaError_t launch_gather_stats(int dtype, int d, const void *x, const int64_t *st, int64_t batch,
