@@ -29,8 +29,11 @@
 //              once per tile through smem + a 64-thread named barrier; online
 //              softmax in the exp2 domain (FFMA2 / FMNMX3 / FADD2), lazy O
 //              rescaling (only when the running max grows by > 2^8), P_u (bf16)
-//              written back over S_u in TMEM; epilogue O / l -> bf16 rows at
-//              pi_q(i), plus optional LSE.
+//              written back over S_u in TMEM in two parts per half, each
+//              signalled at once so that the MMA issuer starts PV_u on it while
+//              the rest is exponentiated; epilogue O / l -> bf16 rows at pi_q(i)
+//              (or every peer buffer: the fused head-parallel gather), plus
+//              optional LSE.
 // The key-block list is turned into an smem bitmask once per CTA (union of
 // the pair's lists for B = 64); every role enumerates its set bits in order.
 // TMEM columns: S0 [0,B), S1 [B,2B), O [256,384), Q [384,448).
@@ -53,7 +56,6 @@ constexpr int HD = 128;          // head dim
 constexpr uint32_t O_COL = 256;
 constexpr uint32_t Q_COL = 384;
 constexpr int kSoftmaxWarp0 = 2;
-constexpr int kVProducerWarp = 10;
 constexpr int kThreads = 352;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kDefaultEmu = 0;             // pairs per 8 on the polynomial exp2 (off: MUFU + power cap wins)
