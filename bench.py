@@ -58,9 +58,11 @@ def parse():
     ap.add_argument("--fused", action="store_true",
                     help="with --shard heads: fuse the output all-gather into the attention epilogue (peer stores "
                          "into symmetric memory, ba_sparse_attn_peers) instead of an NCCL all-gather")
-    ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
+    ap.add_argument("--shard", default="batch", choices=["batch", "heads", "units"],
                     help="batch: weak scaling, rank r runs its own batch element (default); heads: strong "
-                         "scaling, rank r runs a slice of whole GQA groups and O is all-gathered (NCCL)")
+                         "scaling, rank r runs a slice of whole GQA groups and O is all-gathered (NCCL); falls "
+                         "back to units when the KV heads do not divide by the world size; units: strong scaling "
+                         "over evenly split (head, q-block) work units (SURVEY 8(e))")
     return ap.parse_args()
 
 
@@ -128,8 +130,9 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- FLOPs
-def sparse_flops_from_index(kv_index, kv_count, lq, lk, B, d):
-    """Sum over selected pairs of 4 n_q n_k d (QK^T + PV), ragged sizes exact."""
+def sparse_flops_from_index(kv_index, kv_count, lq, lk, B, d, units=None):
+    """Sum over selected pairs of 4 n_q n_k d (QK^T + PV), ragged sizes exact;
+    `units` = (u0, u1) restricts it to the work units u = (b*H + h)*N_q + g_q."""
     import torch
     nq = kv_index.shape[2]
     nk_tot = (lk + B - 1) // B
@@ -140,7 +143,10 @@ def sparse_flops_from_index(kv_index, kv_count, lq, lk, B, d):
     valid = torch.arange(kap, device=kv_index.device)[None, None, None, :] < kv_count[..., None]
     nk_sizes = torch.where(kv_index == nk_tot - 1, float(last_k), float(B)).double() * valid
     per_row = nk_sizes.sum(-1)  # [b, h, nq]
-    return float((per_row * nq_rows[None, None, :]).sum().item()) * 4.0 * d
+    per_unit = (per_row * nq_rows[None, None, :]).flatten()
+    if units is not None:
+        per_unit = per_unit[units[0]:units[1]]
+    return float(per_unit.sum().item()) * 4.0 * d
 
 
 def cpu_cores():
@@ -225,7 +231,8 @@ def run_ours(args):
     import torch.distributed as dist
     from synth import CONFIGS, make_qkv
     import paper_2605_19726_b200.baatt as ba
-    from paper_2605_19726_b200.dist import gather_heads, head_range, max_over_ranks, sum_over_ranks
+    from paper_2605_19726_b200.dist import (even_split, gather_heads, gather_units, head_range, max_over_ranks,
+                                            sum_over_ranks, unit_heads, unit_range)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -239,12 +246,22 @@ def run_ours(args):
     ba.load()
     w = CONFIGS[args.config]
     density = args.density if args.density is not None else w.density
-    heads = args.shard == "heads" and (world > 1 or args.fused)
+    heads = args.shard in ("heads", "units") and (world > 1 or args.fused or args.shard == "units")
     fused = None
+    units = None      # (u0, u1) relative to this rank's head slice in the uneven head split
+    out_full = None   # zero-filled full O of the NCCL unit-split reassembly
     if heads:
         # strong scaling: every rank builds the same problem and keeps whole GQA groups
         q, k, v = make_qkv(w, device=dev)
-        q0, q1, k0, k1 = head_range(w.heads_q, w.heads_kv, world, rank)
+        if args.shard == "heads" and even_split(w.heads_q, w.heads_kv, world):
+            q0, q1, k0, k1 = head_range(w.heads_q, w.heads_kv, world, rank)
+        else:
+            # SURVEY §8(e) fallback (e.g. M's 28 heads on 8 GPUs): split the flattened (head, q-block)
+            # units evenly; a rank selects over the heads its units touch (whole GQA groups)
+            nq_full = (w.seq_len + w.block_size - 1) // w.block_size
+            u0, u1 = unit_range(w.heads_q, nq_full, world, rank)
+            q0, q1, k0, k1 = unit_heads(u0, u1, nq_full, w.heads_q, w.heads_kv)
+            units = (u0 - q0 * nq_full, u1 - q0 * nq_full)
         q, k, v = q[:, q0:q1].contiguous(), k[:, k0:k1].contiguous(), v[:, k0:k1].contiguous()
     else:
         # weak scaling: rank r processes batch element r (its own seeded inputs)
@@ -261,22 +278,36 @@ def run_ours(args):
         from paper_2605_19726_b200.dist import FusedHeadGather
         fused = FusedHeadGather((q.shape[0], w.heads_q, q.shape[2], q.shape[3]), q.dtype, dev, q0)
         out = fused.full[:, q0:q1]
+    elif units is not None:
+        out_full = torch.zeros((q.shape[0], w.heads_q, q.shape[2], q.shape[3]), dtype=q.dtype, device=dev)
+        out = out_full[:, q0:q1]
     else:
         out = torch.empty_like(q)
     ctx = ba.Context(q, k, v, w.block_size, density, 1.0, "qk", args.comp, top_p=args.top_p, zero_copy=zero_copy,
                      out=out)
     stream = torch.cuda.current_stream()
 
-    def attn_and_gather():
-        if fused is not None:
+    def attn():
+        if units is not None:
+            ctx.sparse_attn_units(units[0], units[1], fused.peer_ptrs if fused is not None else [out])
+        elif fused is not None:
             ctx.sparse_attn_peers(fused.peer_ptrs)
-            n = ba.last_launch_count()
+        else:
+            ctx.sparse_attn(out)
+
+    def gather():
+        if fused is not None:
             fused.barrier()
-            return n
-        ctx.sparse_attn(out)
-        n = ba.last_launch_count()
-        if heads:
+        elif units is not None:
+            if world > 1:
+                gather_units(out_full)  # every row has one writer: SUM all-reduce of the zero-filled O
+        elif heads:
             gather_heads(out, w.heads_q)  # the path's only collective (NCCL all-gather over NVLink)
+
+    def attn_and_gather():
+        attn()
+        n = ba.last_launch_count()
+        gather()
         return n
 
     def step():
@@ -288,7 +319,7 @@ def run_ours(args):
         launches = step()
     torch.cuda.synchronize()
     flops_per_step = sparse_flops_from_index(ctx.sel.kv_index, ctx.sel.kv_count, q.shape[2], k.shape[2],
-                                             w.block_size, w.head_dim)
+                                             w.block_size, w.head_dim, units)
     sampler = ClockSampler(local) if not args.profile else None
     if sampler:
         sampler.start()
@@ -305,15 +336,9 @@ def run_ours(args):
         ev[i][0].record(stream)
         ctx.select(q, k, v)
         ev[i][1].record(stream)
-        if fused is not None:
-            ctx.sparse_attn_peers(fused.peer_ptrs)
-            ev[i][2].record(stream)
-            fused.barrier()
-        else:
-            ctx.sparse_attn(out)
-            ev[i][2].record(stream)
-            if heads:
-                gather_heads(out, w.heads_q)
+        attn()
+        ev[i][2].record(stream)
+        gather()
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -444,7 +469,11 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": workload_desc(w, density, args.top_p, args.comp), "global_batch": 1 if heads else world,
                        "seq_len": w.seq_len,
-                       "parallelism": (f"head-parallel x{world} (whole GQA groups per rank, "
+                       "parallelism": (f"unit-parallel x{world} ((head, q-block) units split evenly, "
+                                       + ("O by peer stores in the attention epilogue)" if fused is not None
+                                          else "NCCL SUM all-reduce of the zero-filled O)")
+                                       if units is not None else
+                                       f"head-parallel x{world} (whole GQA groups per rank, "
                                        + ("O gathered by peer stores in the attention epilogue)" if fused is not None
                                           else "NCCL all-gather of O)")
                                        if heads else f"batch-parallel x{world} (weak scaling, no data-path collective)"),

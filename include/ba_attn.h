@@ -218,6 +218,30 @@ ba_status ba_sparse_attn_peers(const ba_problem *prob, const ba_params *params,
                                const ba_selection *sel, void *const *out_peers, int n_peers,
                                float *lse, cudaStream_t stream);
 
+/* Alg. 1 steps 11-12 for a contiguous range of WORK UNITS only —
+ * the uneven multi-GPU split of SURVEY §8(e) (e.g. 28 heads over 8 GPUs):
+ * unit u = (b*H_q + h)*N_q + g_q is query block g_q of head h of batch b, and
+ * every row of the units in [unit_begin, unit_end) is computed as
+ * ba_sparse_attn computes it and stored at its ORIGINAL token position in
+ * each of out[0..n_out); rows of other units are not written.  Bit-identical
+ * to ba_sparse_attn when both range ends fall on an even query block or a
+ * head boundary: the B = 64 dual-tile kernel pairs query blocks (2p, 2p+1)
+ * and groups key blocks by the pair's union, so a block's rounding depends
+ * on its partner (the B = 128 kernels' rows depend only on their own list);
+ * otherwise equal within the parity tolerance.  Every (b, h) problem
+ * is independent (Alg. 1 is per head), so rank r of G can run units
+ * [r*U/G, (r+1)*U/G) after a ba_select over the heads it touches.  n_out = 1:
+ * plain stores (any kernel); 1 < n_out <= 8: peer stores as
+ * ba_sparse_attn_peers (same kernel requirements; the caller synchronises the
+ * peers).  Reads the permuted copies, kv_index, kv_count, perm_q.  lse as
+ * ba_sparse_attn (only the units' rows written).  Launches one kernel per run
+ * of whole GQA groups and one per partial head.  Errors: range outside
+ * [0, b*H_q*N_q) or n_out outside 1..8 -> BA_ERR_INVALID_ARGUMENT; an empty
+ * range enqueues nothing and returns BA_OK. */
+ba_status ba_sparse_attn_units(const ba_problem *prob, const ba_params *params,
+                               const ba_selection *sel, int64_t unit_begin, int64_t unit_end,
+                               void *const *out, int n_out, float *lse, cudaStream_t stream);
+
 /* ba_select + attention with the selection carved from the workspace
  * (>= ba_attention_workspace_size bytes), on the permuted copies
  * (ba_sparse_attn) — the faster path on B200.  The environment

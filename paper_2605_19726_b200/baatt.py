@@ -88,6 +88,9 @@ def load() -> ctypes.CDLL:
     lib.ba_block_mass.restype = ctypes.c_int
     lib.ba_sparse_attn_peers.argtypes = [P, PA, S, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, vp, st]
     lib.ba_sparse_attn_peers.restype = ctypes.c_int
+    lib.ba_sparse_attn_units.argtypes = [P, PA, S, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p),
+                                         ctypes.c_int, vp, st]
+    lib.ba_sparse_attn_units.restype = ctypes.c_int
     lib.ba_zero_copy_supported.argtypes = [P, PA]
     lib.ba_zero_copy_supported.restype = ctypes.c_int
     lib.ba_attention.argtypes = [P, PA, vp, vp, vp, vp, vp, vp, sz, st]
@@ -107,7 +110,8 @@ def load() -> ctypes.CDLL:
 
 
 EXPORTED = ["ba_abi_version", "ba_selection_sizes", "ba_select_workspace_size", "ba_attention_workspace_size",
-            "ba_select", "ba_sparse_attn", "ba_sparse_attn_gather", "ba_sparse_attn_peers", "ba_zero_copy_supported",
+            "ba_select", "ba_sparse_attn", "ba_sparse_attn_gather", "ba_sparse_attn_peers", "ba_sparse_attn_units",
+            "ba_zero_copy_supported",
             "ba_attention", "ba_dense_attn", "ba_block_mass_workspace_size", "ba_block_mass",
             "ba_attention_host_workspace_size", "ba_attention_host", "ba_last_launch_count",
             "ba_attention_kernel_name",
@@ -310,6 +314,16 @@ class Context:
         arr = (ctypes.c_void_p * len(peer_ptrs))(*[ctypes.c_void_p(int(p)) for p in peer_ptrs])
         _check(load().ba_sparse_attn_peers(ctypes.byref(self.prob), ctypes.byref(self.params), ctypes.byref(self.sel_c),
                                            arr, len(peer_ptrs), _ptr(lse), _stream(stream)))
+
+    def sparse_attn_units(self, unit_begin: int, unit_end: int, outs, lse=None, stream=None):
+        """Attention for work units [unit_begin, unit_end) only, u = (b*Hq + h)*Nq + g_q
+        (ba_sparse_attn_units): rows stored at their original positions in every
+        output of `outs` (tensors or device pointers; strides those of `out` given
+        at construction)."""
+        ptrs = [o.data_ptr() if isinstance(o, torch.Tensor) else int(o) for o in outs]
+        arr = (ctypes.c_void_p * len(ptrs))(*[ctypes.c_void_p(p) for p in ptrs])
+        _check(load().ba_sparse_attn_units(ctypes.byref(self.prob), ctypes.byref(self.params), ctypes.byref(self.sel_c),
+                                           int(unit_begin), int(unit_end), arr, len(ptrs), _ptr(lse), _stream(stream)))
 
     def sparse_attn(self, out, lse=None, sel: Optional[Selection] = None, stream=None):
         sc = self.sel_c if sel is None else sel.to_c()

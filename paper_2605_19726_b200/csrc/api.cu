@@ -523,6 +523,79 @@ ba_status ba_sparse_attn_peers(const ba_problem *prob, const ba_params *params, 
   return run_attn(a, stream);
 }
 
+// Work units: u = (b*H_q + h)*N_q + g_q.  A range [u0, u1) is
+// cut into segments — runs of whole heads of one batch element covering whole
+// GQA groups, else one (partial) head — and each segment runs as a
+// sub-problem whose pointers are advanced to its first head / query block:
+// the kernels index Q', kv_index, kv_count and perm_q relative to those
+// pointers and write out / lse through perm_q (original token indices), so a
+// sub-problem writes exactly its own rows of the full-size output.
+ba_status ba_sparse_attn_units(const ba_problem *prob, const ba_params *params, const ba_selection *sel,
+                               int64_t unit_begin, int64_t unit_end, void *const *out, int n_out, float *lse,
+                               cudaStream_t stream) {
+  g_err.clear();
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  const int64_t n_units = D.b * D.hq * D.nq;
+  if (unit_begin < 0 || unit_end < unit_begin || unit_end > n_units)
+    return fail(BA_ERR_INVALID_ARGUMENT, "unit range [%lld, %lld) not within [0, %lld)", (long long)unit_begin,
+                (long long)unit_end, (long long)n_units);
+  if (!out || n_out < 1 || n_out > kMaxPeers)
+    return fail(BA_ERR_INVALID_ARGUMENT, "n_out = %d (1..%d) / out NULL", n_out, kMaxPeers);
+  for (int p = 0; p < n_out; ++p) {
+    char name[32];
+    snprintf(name, sizeof(name), "out[%d]", p);
+    BA_TRY(check_ptr(name, out[p]));
+  }
+  if (!sel || !sel->q_sorted || !sel->k_sorted || !sel->v_sorted || !sel->kv_index || !sel->kv_count || !sel->perm_q)
+    return fail(BA_ERR_INVALID_ARGUMENT, "ba_sparse_attn_units reads the permuted copies, kv_index, kv_count, perm_q");
+  BA_TRY(check_strides("o", prob->o_stride, D.esz));
+  AttnArgs base = make_attn(D, params);
+  if (n_out > 1 && (!attn_sm100_supported(base) || use_pps(base) || use_2cta(base)))
+    return fail(BA_ERR_UNSUPPORTED, "peer stores need the bf16 tcgen05 pair / single-CTA kernels (d = 128)");
+  base.q = sel->q_sorted; base.k = sel->k_sorted; base.v = sel->v_sorted;
+  base.qs[0] = D.hq * D.lq * D.d; base.qs[1] = D.lq * D.d; base.qs[2] = D.d;
+  base.ks[0] = D.hkv * D.lk * D.d; base.ks[1] = D.lk * D.d; base.ks[2] = D.d;
+  for (int i = 0; i < 3; ++i) { base.vs[i] = base.ks[i]; base.os[i] = prob->o_stride[i]; }
+  base.kv_stride = D.kappa;
+  const int64_t grp = D.hq / D.hkv;
+  int launches = 0;
+  for (int64_t u = unit_begin; u < unit_end;) {
+    const int64_t bh = u / D.nq, g0 = u % D.nq, b = bh / D.hq, h0 = bh % D.hq;
+    int64_t nh = 1, g1 = std::min<int64_t>(D.nq, g0 + (unit_end - u));
+    if (g0 == 0 && g1 == D.nq && h0 % grp == 0) {  // whole heads: extend over whole GQA groups of batch b
+      const int64_t whole = std::min<int64_t>((unit_end - u) / D.nq, D.hq - h0);
+      if (whole >= grp) nh = whole / grp * grp;
+    }
+    AttnArgs a = base;
+    const int64_t lq0 = g0 * D.B, lq1 = std::min<int64_t>(D.lq, g1 * D.B);
+    a.batch = 1;
+    a.hq = nh;
+    a.hkv = nh == 1 ? 1 : nh / grp;
+    a.lq = nh == 1 ? lq1 - lq0 : D.lq;
+    a.nq = g1 - g0;
+    a.q = static_cast<const char *>(base.q) + (b * base.qs[0] + h0 * base.qs[1] + lq0 * base.qs[2]) * D.esz;
+    const int64_t koff = (b * base.ks[0] + (h0 / grp) * base.ks[1]) * D.esz;
+    a.k = static_cast<const char *>(base.k) + koff;
+    a.v = static_cast<const char *>(base.v) + koff;
+    a.kv_index = sel->kv_index + ((b * D.hq + h0) * D.nq + g0) * D.kappa;
+    a.kv_count = sel->kv_count + (b * D.hq + h0) * D.nq + g0;
+    a.perm_q = sel->perm_q + (b * D.hq + h0) * D.lq + lq0;
+    a.lse = lse ? lse + (b * D.hq + h0) * D.lq : nullptr;
+    const int64_t ooff = (b * prob->o_stride[0] + h0 * prob->o_stride[1]) * D.esz;
+    a.out = static_cast<char *>(out[0]) + ooff;
+    if (n_out > 1) {
+      a.n_peers = n_out;
+      for (int p = 0; p < n_out; ++p) a.out_peers[p] = static_cast<char *>(out[p]) + ooff;
+    }
+    BA_TRY(run_attn(a, stream));
+    ++launches;
+    u += nh == 1 ? g1 - g0 : nh * D.nq;
+  }
+  g_launches = launches;
+  return BA_OK;
+}
+
 ba_status ba_attention(const ba_problem *prob, const ba_params *params, const void *q, const void *k,
                        const void *v, void *out, float *lse, void *workspace, size_t workspace_bytes,
                        cudaStream_t stream) {

@@ -35,6 +35,43 @@ def even_split(heads_q: int, heads_kv: int, world: int) -> bool:
     return heads_kv % world == 0
 
 
+def unit_range(heads: int, n_q: int, world: int, rank: int, pair: int = 2) -> Tuple[int, int]:
+    """[u0, u1): rank's share of the flattened work units u = (b*Hq + h)*Nq + g_q
+    (SURVEY §8(e) fallback when the heads do not divide by the world size, e.g.
+    M's 28 heads on 8 GPUs).  Contiguous; boundaries fall on pairs of query
+    blocks (2p, 2p+1) of a head — the tiles the attention kernels pair — so the
+    reassembled output is bit-identical to one GPU's; shares differ by at most
+    one pair.  `heads` = b*Hq for batched problems."""
+    n_p = (n_q + pair - 1) // pair
+    base, extra = divmod(heads * n_p, world)
+    p0 = rank * base + min(rank, extra)
+    p1 = p0 + base + (1 if rank < extra else 0)
+
+    def unit(p):
+        return (p // n_p) * n_q + min(pair * (p % n_p), n_q)
+    return unit(p0), unit(p1)
+
+
+def unit_heads(u0: int, u1: int, n_q: int, heads_q: int, heads_kv: int) -> Tuple[int, int, int, int]:
+    """(q0, q1, kv0, kv1): the head span (batch 1) a rank must select over to
+    run units [u0, u1) — the q-heads they touch, widened to whole GQA groups so
+    that the K'/V' copies of every KV head it reads are its own."""
+    grp = heads_q // heads_kv
+    if u1 <= u0:
+        return 0, 0, 0, 0
+    h0, h1 = u0 // n_q, (u1 - 1) // n_q + 1
+    kv0, kv1 = h0 // grp, (h1 + grp - 1) // grp
+    return kv0 * grp, kv1 * grp, kv0, kv1
+
+
+def gather_units(out_full: torch.Tensor, group=None) -> torch.Tensor:
+    """Reassemble O after a unit split: every rank stored its units' rows into a
+    zero-filled full-size O and every row has exactly one writer, so a SUM
+    all-reduce reproduces the 1-GPU output bit for bit (x + 0 is exact)."""
+    dist.all_reduce(out_full, op=dist.ReduceOp.SUM, group=group)
+    return out_full
+
+
 def gather_heads(out_local: torch.Tensor, heads_q: int, group=None) -> torch.Tensor:
     """Reassemble O [b, Hq, L, d] from per-rank head slices [b, Hq_r, L, d].
     Uses one all_gather_into_tensor when every rank holds the same number of

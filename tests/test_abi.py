@@ -172,3 +172,22 @@ def test_exact_compensation_workspace(ba):
     exact = lib.ba_select_workspace_size(ctypes.byref(p), ctypes.byref(ba.make_params(comp="exact")))
     n = 2048 // 128
     assert exact - diag >= 8 * 128 * 128 * n * (4 + 2)
+
+
+def test_units_validation_before_launch(ba):
+    """ba_sparse_attn_units checks its unit range and output list synchronously
+    (nothing is launched, so this runs without a GPU)."""
+    q, k, v = _meta(1, 4, 2, 1000, 128)
+    p, pa = ba.make_problem(q, k, v), ba.make_params()
+    lib = ba.load()
+    sel = ba.SelectionC()
+    n_units = 4 * ((1000 + 127) // 128)
+    outs = (ctypes.c_void_p * 1)(ctypes.c_void_p(256))
+    for u0, u1 in ((-1, 3), (5, 4), (0, n_units + 1)):
+        st = lib.ba_sparse_attn_units(ctypes.byref(p), ctypes.byref(pa), ctypes.byref(sel), u0, u1, outs, 1, None, None)
+        assert lib.ba_status_string(st).decode() == "BA_ERR_INVALID_ARGUMENT"
+        assert b"unit range" in lib.ba_last_error()
+    st = lib.ba_sparse_attn_units(ctypes.byref(p), ctypes.byref(pa), ctypes.byref(sel), 0, n_units, outs, 9, None, None)
+    assert b"n_out" in lib.ba_last_error()
+    st = lib.ba_sparse_attn_units(ctypes.byref(p), ctypes.byref(pa), ctypes.byref(sel), 0, n_units, outs, 1, None, None)
+    assert lib.ba_status_string(st).decode() == "BA_ERR_INVALID_ARGUMENT"  # empty selection struct

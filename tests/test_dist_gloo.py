@@ -13,7 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2605_19726_b200.dist import gather_heads, head_range, max_over_ranks, sum_over_ranks
+from paper_2605_19726_b200.dist import (gather_heads, gather_units, head_range, max_over_ranks, sum_over_ranks,
+                                        unit_heads, unit_range)
 
 
 def test_head_range_partitions():
@@ -86,3 +87,62 @@ def test_peer_slice_ptrs():
             # the local head h of this rank lands on global head q0 + h of every copy
             h = q1 - q0 - 1
             assert ptrs[0] + h * full.stride(1) * 2 == bases[0] + (q0 + h) * L * d * 2
+
+
+def test_unit_range_partitions():
+    """SURVEY §8(e) uneven split: flattened (head, q-block) units, contiguous,
+    balanced to one unit, every unit owned once; the head span a rank selects
+    over covers its units with whole GQA groups."""
+    for hq, hkv, nq in ((28, 28, 1024), (32, 8, 1024), (24, 24, 591), (6, 3, 7), (1, 1, 16)):
+        for world in (1, 2, 3, 4, 5, 8):
+            owned, sizes = [], []
+            for r in range(world):
+                u0, u1 = unit_range(hq, nq, world, r)
+                owned += list(range(u0, u1))
+                sizes.append(u1 - u0)
+                assert u0 % nq % 2 == 0  # starts on a q-block pair (2p, 2p+1)
+                q0, q1, k0, k1 = unit_heads(u0, u1, nq, hq, hkv)
+                grp = hq // hkv
+                if u1 > u0:
+                    assert q0 <= u0 // nq and (u1 - 1) // nq < q1
+                    assert q0 == k0 * grp and q1 == k1 * grp
+            assert owned == list(range(hq * nq))
+            # one pair, plus the one-block tail pairs of odd N_q (at most one per head a rank touches)
+            assert max(sizes) - min(sizes) <= 2 + (nq % 2) * (hq // world + 2)
+    # M on 8 GPUs: 3.5 heads of work per rank instead of 4/4/4/4/3/3/3/3 (speedup cap 7.0x -> 8x)
+    sizes = [unit_range(28, 1024, 8, r)[1] - unit_range(28, 1024, 8, r)[0] for r in range(8)]
+    assert sizes == [3584] * 8
+
+
+def _unit_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        hq, L, d, B = 5, 37, 4, 8  # ragged last block, 5 heads over 3 ranks
+        nq = (L + B - 1) // B
+        g = torch.Generator().manual_seed(7)
+        full = torch.randn(1, hq, L, d, generator=g)
+        perm = torch.stack([torch.randperm(L, generator=g) for _ in range(hq)])  # sorted position -> token
+        u0, u1 = unit_range(hq, nq, world, rank)
+        mine = torch.zeros_like(full)
+        for u in range(u0, u1):  # what ba_sparse_attn_units stores: the unit's rows at pi_q positions
+            h, gq = divmod(u, nq)
+            rows = perm[h, gq * B:min(L, (gq + 1) * B)]
+            mine[0, h, rows] = full[0, h, rows]
+        got = gather_units(mine)
+        q.put((rank, torch.equal(got, full)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_units_world3():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_unit_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res

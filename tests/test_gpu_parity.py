@@ -480,3 +480,65 @@ def test_sparse_attn_peers_broadcast(ba, cfg, L, hq, hkv, B):
     for f in fulls:
         assert torch.equal(f[:, hq:], ref)
         assert torch.isnan(f[:, :hq].float()).all()  # nothing written outside this rank's heads
+
+
+# ---------------------------------------------------------------- uneven split: work units
+@pytest.mark.parametrize("cfg,L,hq,hkv,B", [("C", 2048 + 64, 8, 2, 128), ("M", 2048 + 33, 5, 5, 64),
+                                            ("T", 1000, 3, 3, 64)])
+@pytest.mark.parametrize("world", [3, 8])
+def test_sparse_attn_units_reassemble_bitwise(ba, cfg, L, hq, hkv, B, world):
+    """Each simulated rank selects over the heads its units touch (whole GQA
+    groups) and runs ba_sparse_attn_units on its unit range; the union of the
+    ranks' rows is the 1-GPU ba_sparse_attn output and LSE, bit for bit."""
+    from paper_2605_19726_b200.dist import unit_heads, unit_range
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv)
+    ref, lse_ref = torch.empty_like(q), torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+    ctx0 = ba.Context(q, k, v, B, 0.5)
+    ctx0.select(q, k, v)
+    ctx0.sparse_attn(ref, lse_ref)
+    nq = ctx0.sel.n_q
+    out = torch.full_like(q, float("nan"))
+    lse = torch.full_like(lse_ref, float("nan"))
+    for r in range(world):
+        u0, u1 = unit_range(hq, nq, world, r)
+        q0, q1, k0, k1 = unit_heads(u0, u1, nq, hq, hkv)
+        if u1 <= u0:
+            continue
+        qs, ks, vs = q[:, q0:q1].contiguous(), k[:, k0:k1].contiguous(), v[:, k0:k1].contiguous()
+        ctx = ba.Context(qs, ks, vs, B, 0.5, out=out[:, q0:q1])
+        ctx.select(qs, ks, vs)
+        ctx.sparse_attn_units(u0 - q0 * nq, u1 - q0 * nq, [out[:, q0:q1]], lse=lse[:, q0:q1])
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    assert torch.equal(lse, lse_ref)
+
+
+def test_sparse_attn_units_batch_and_peers(ba):
+    """Unit ranges crossing head and batch boundaries of one selection (b = 2,
+    GQA) cover the output exactly once; with two outputs every row lands in
+    both (the peer-store path)."""
+    w = CONFIGS["C"]
+    B, L, hq, hkv = 128, 1536 + 40, 4, 2
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv, batch=2)
+    ref = torch.empty_like(q)
+    ctx = ba.Context(q, k, v, B, 0.5)
+    ctx.select(q, k, v)
+    ctx.sparse_attn(ref)
+    nq = ctx.sel.n_q
+    n = 2 * hq * nq
+    cuts = [0, 5, nq, nq + 1, 3 * nq - 2, 5 * nq + 3, n]
+    outs = [torch.full_like(q, float("nan")) for _ in range(2)]
+    for a, b_ in zip(cuts[:-1], cuts[1:]):
+        ctx.sparse_attn_units(a, b_, outs[:1])
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], ref)
+    outs[0].fill_(float("nan"))
+    for a, b_ in zip(cuts[:-1], cuts[1:]):
+        ctx.sparse_attn_units(a, b_, outs)
+    ctx.sparse_attn_units(n, n, outs)  # empty range: nothing enqueued
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, ref)
+    with pytest.raises(ba.BaError):
+        ctx.sparse_attn_units(0, n + 1, outs[:1])
