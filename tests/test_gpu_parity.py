@@ -182,14 +182,16 @@ def test_injected_oracle_mask(ba):
     assert ref_sel  # oracle selection computed on the same inputs
 
 
-@pytest.mark.parametrize("B,k5", [(128, "1cta"), (128, "2cta"), (128, "pp"), (128, "pps"), (64, "dual"), (64, "pair")])
+@pytest.mark.parametrize("B,k5", [(128, "1cta"), (128, "2cta"), (128, "pp"), (128, "ppseq"), (128, "pps"), (64, "dual"),
+                                  (64, "pair")])
 def test_injected_dissimilar_lists(ba, B, k5):
     """Random (dissimilar) index lists for every query block: exercises the
     pair kernels' union walk where a block skips tiles (P = 0 rows), including
     a skipped LAST tile (the epilogue must still wait for every PV), and for
     B = 64 odd union lengths (the dual kernel's half-empty last tile)."""
     import subprocess, sys, os
-    env = dict(os.environ, **({"BA_ATTN_K5": k5} if B == 128 else {"BA_ATTN_B64": k5}))
+    env = dict(os.environ, **({"BA_ATTN_K5": k5.replace("seq", "")} if B == 128 else {"BA_ATTN_B64": k5}))
+    env["BA_PP_SEQ"] = "1" if k5 == "ppseq" else "0"
     code = f"""
 import sys; sys.path.insert(0, {os.path.join(os.path.dirname(__file__))!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
 import numpy as np, torch
@@ -241,12 +243,13 @@ def test_errors_are_loud(ba):
 
 
 @pytest.mark.parametrize("k5,name", [("2cta", "attn_sm100_tcgen05_2cta"), ("pp", "attn_sm100_tcgen05_pp"),
-                                     ("pps", "attn_sm100_tcgen05_pps"), ("1cta", "attn_sm100_tcgen05")])
+                                     ("ppseq", "attn_sm100_tcgen05_pp"), ("pps", "attn_sm100_tcgen05_pps"),
+                                     ("1cta", "attn_sm100_tcgen05")])
 def test_b128_kernel_parity(ba, k5, name):
     """Each B = 128 kernel (BA_ATTN_K5 = 2cta | pp | 1cta) on real selections,
     ragged lengths, GQA and an odd number of query blocks."""
     import os, subprocess, sys
-    env = dict(os.environ, BA_ATTN_K5=k5)
+    env = dict(os.environ, BA_ATTN_K5=k5.replace("seq", ""), BA_PP_SEQ="1" if k5 == "ppseq" else "0")
     code = f"""
 import sys; sys.path.insert(0, {os.path.dirname(__file__)!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
 import torch
