@@ -552,13 +552,16 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
           for (int i = 0; i < 128; ++i)
             if (i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
         }
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        // row max: 8 independent FMNMX3 chains of depth 8 (the lone warp's latency, not its issue, bounds this)
+        float m8[8];
 #pragma unroll
-        for (int i = 0; i < 128; i += 8) {
+        for (int v = 0; v < 8; ++v) m8[v] = fmaxf(__uint_as_float(sr[2 * v]), __uint_as_float(sr[2 * v + 1]));
 #pragma unroll
-          for (int v = 0; v < 4; ++v) m4[v] = fmax3(m4[v], __uint_as_float(sr[i + 2 * v]), __uint_as_float(sr[i + 2 * v + 1]));
+        for (int i = 16; i < 128; i += 16) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v) m8[v] = fmax3(m8[v], __uint_as_float(sr[i + 2 * v]), __uint_as_float(sr[i + 2 * v + 1]));
         }
-        const float mt = fmaxf(fmax3(m4[0], m4[1], m4[2]), m4[3]) * c;
+        const float mt = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7])) * c;
         if (m == -INFINITY) {
           m = mt;  // first tile of these rows: O rows are still zero (earlier P rows were 0)
         } else {
