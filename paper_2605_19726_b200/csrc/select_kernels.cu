@@ -351,25 +351,27 @@ cudaError_t launch_radix_sort(const SortGeom &g, uint32_t *keys_a, uint32_t *val
 // which the two-pass form saturated), and the shift keeps the cancellation at
 // eps * (var + (mean - K)^2) instead of eps * (var + mean^2).
 // =====================================================================================
-template <typename T, int D>
+template <typename T, int D, int NBLK = 1>
 BA_DEVICE void gather_stats_body(const T *__restrict__ x, int64_t s0, int64_t s1, int64_t s2, int64_t heads, int64_t L,
                                  int B, const int32_t *__restrict__ perm, int32_t *__restrict__ perm_id_out,
-                                 T *__restrict__ xs, double *__restrict__ mean, double *__restrict__ var, int64_t g,
+                                 T *__restrict__ xs, double *__restrict__ mean, double *__restrict__ var, int64_t gp,
                                  int64_t bh) {
+  // NBLK blocks per CTA (NBLK * B <= 128 rows): B = 64 runs two blocks per CTA so that as
+  // many row loads are in flight per SM as at B = 128; the moments are per block
   constexpr int EPC = Chunk<T>::EPC;
   constexpr int CPR = D / EPC;       // chunks per row
   constexpr int RPI = 256 / CPR;     // rows per iteration
-  constexpr int MAXIT = 128 / RPI;   // B <= 128
+  constexpr int MAXIT = 128 / RPI;   // NBLK * B <= 128
   static_assert(CPR * 2 == 32 || CPR == 32 || CPR * 4 == 32, "row groups per warp");
   constexpr int GPW = 32 / CPR;                 // row groups per warp (combined by shuffles)
   constexpr int RG = RPI / GPW;                 // partial rows left for the smem reduction
   __shared__ double red[2][RG][D + 1];
   __shared__ double s_shift[D];
-  const int64_t b = bh / heads, h = bh - b * heads;  // g: block, bh: batch * heads + head
+  const int64_t b = bh / heads, h = bh - b * heads;  // gp: block group, bh: batch * heads + head
   const int chunk = threadIdx.x % CPR;
   const int rsub = threadIdx.x / CPR;
-  const int64_t row0 = g * B;
-  const int n = (int)imin64(B, L - row0);
+  const int64_t row0 = gp * NBLK * B;
+  const int n = (int)imin64((int64_t)NBLK * B, L - row0);
   const T *xbase = x + b * s0 + h * s1 + chunk * EPC;
   T *xsbase = xs ? xs + (bh * L + row0) * D + chunk * EPC : nullptr;
   // stage 1: source row indices; stage 2: every row load in flight; stage 3: stores + sums
@@ -392,8 +394,9 @@ BA_DEVICE void gather_stats_body(const T *__restrict__ x, int64_t s0, int64_t s1
 #pragma unroll
   for (int it = 0; it < MAXIT; ++it)
     raw[it] = src[it] >= 0 ? ldg16(xbase + (int64_t)src[it] * s2) : make_uint4(0, 0, 0, 0);
-  uint4 kraw = make_uint4(0, 0, 0, 0);
-  if (mean) kraw = ldg16(xbase + (int64_t)(perm ? __ldg(perm + bh * L + row0) : (int32_t)row0) * s2);  // shift row
+  // shift row of the first block = its first row (loaded before the copy stores, like the rows)
+  uint4 kraw0 = make_uint4(0, 0, 0, 0);
+  if (mean) kraw0 = ldg16(xbase + (int64_t)(perm ? __ldg(perm + bh * L + row0) : (int32_t)row0) * s2);
   if (xs) {  // permuted copy (NULL: zero-copy attention reads the rows through pi itself)
 #pragma unroll
     for (int it = 0; it < MAXIT; ++it) {
@@ -402,53 +405,63 @@ BA_DEVICE void gather_stats_body(const T *__restrict__ x, int64_t s0, int64_t s1
     }
   }
   if (!mean) return;  // V: copy only
-  double kc[EPC], a1[EPC], a2[EPC];
-  {
-    float v[EPC];
-    Chunk<T>::unpack(kraw, v);
-#pragma unroll
-    for (int e = 0; e < EPC; ++e) { kc[e] = (double)v[e]; a1[e] = 0.0; a2[e] = 0.0; }
-  }
-#pragma unroll
-  for (int it = 0; it < MAXIT; ++it) {
-    const int r = rsub + it * RPI;
-    if (r < n) {
+  const int64_t nb = (L + B - 1) / B;
+#pragma unroll 1
+  for (int sb = 0; sb < NBLK; ++sb) {
+    const int64_t g = gp * NBLK + sb;
+    if (g >= nb) break;  // CTA-uniform
+    const int r_lo = sb * B;
+    const int nsb = (int)imin64(B, L - g * B);
+    if (sb > 0) __syncthreads();  // red / s_shift reuse
+    // shift row = the block's first row
+    const uint4 kraw = sb == 0 ? kraw0 : ldg16(xbase + (int64_t)(perm ? __ldg(perm + bh * L + g * B) : (int32_t)(g * B)) * s2);
+    double kc[EPC], a1[EPC], a2[EPC];
+    {
       float v[EPC];
-      Chunk<T>::unpack(raw[it], v);
+      Chunk<T>::unpack(kraw, v);
 #pragma unroll
-      for (int e = 0; e < EPC; ++e) {
-        const double dv = (double)v[e] - kc[e];
-        a1[e] += dv;
-        a2[e] = fma(dv, dv, a2[e]);
+      for (int e = 0; e < EPC; ++e) { kc[e] = (double)v[e]; a1[e] = 0.0; a2[e] = 0.0; }
+    }
+#pragma unroll
+    for (int it = 0; it < MAXIT; ++it) {
+      const int r = rsub + it * RPI;
+      if (r >= r_lo && r < r_lo + nsb) {
+        float v[EPC];
+        Chunk<T>::unpack(raw[it], v);
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const double dv = (double)v[e] - kc[e];
+          a1[e] += dv;
+          a2[e] = fma(dv, dv, a2[e]);
+        }
       }
     }
-  }
 #pragma unroll
-  for (int e = 0; e < EPC; ++e) {
+    for (int e = 0; e < EPC; ++e) {
 #pragma unroll
-    for (int off = CPR; off < 32; off <<= 1) {
-      a1[e] += __shfl_xor_sync(0xffffffffu, a1[e], off);
-      a2[e] += __shfl_xor_sync(0xffffffffu, a2[e], off);
+      for (int off = CPR; off < 32; off <<= 1) {
+        a1[e] += __shfl_xor_sync(0xffffffffu, a1[e], off);
+        a2[e] += __shfl_xor_sync(0xffffffffu, a2[e], off);
+      }
     }
-  }
-  if ((threadIdx.x & 31) < CPR) {
+    if ((threadIdx.x & 31) < CPR) {
 #pragma unroll
-    for (int e = 0; e < EPC; ++e) { red[0][rsub / GPW][chunk * EPC + e] = a1[e]; red[1][rsub / GPW][chunk * EPC + e] = a2[e]; }
-  }
-  if (rsub == 0) {
+      for (int e = 0; e < EPC; ++e) { red[0][rsub / GPW][chunk * EPC + e] = a1[e]; red[1][rsub / GPW][chunk * EPC + e] = a2[e]; }
+    }
+    if (rsub == 0) {
 #pragma unroll
-    for (int e = 0; e < EPC; ++e) s_shift[chunk * EPC + e] = kc[e];
-  }
-  __syncthreads();
-  const double inv_n = 1.0 / (double)n;
-  const int64_t nb = (L + B - 1) / B;
-  for (int c = threadIdx.x; c < D; c += 256) {
-    double t1 = 0.0, t2 = 0.0;
+      for (int e = 0; e < EPC; ++e) s_shift[chunk * EPC + e] = kc[e];
+    }
+    __syncthreads();
+    const double inv_n = 1.0 / (double)nsb;
+    for (int c = threadIdx.x; c < D; c += 256) {
+      double t1 = 0.0, t2 = 0.0;
 #pragma unroll
-    for (int i = 0; i < RG; ++i) { t1 += red[0][i][c]; t2 += red[1][i][c]; }
-    const double m1 = t1 * inv_n;
-    mean[(bh * nb + g) * D + c] = s_shift[c] + m1;
-    var[(bh * nb + g) * D + c] = fmax(fma(-m1, m1, t2 * inv_n), 0.0);
+      for (int i = 0; i < RG; ++i) { t1 += red[0][i][c]; t2 += red[1][i][c]; }
+      const double m1 = t1 * inv_n;
+      mean[(bh * nb + g) * D + c] = s_shift[c] + m1;
+      var[(bh * nb + g) * D + c] = fmax(fma(-m1, m1, t2 * inv_n), 0.0);
+    }
   }
 }
 
@@ -462,26 +475,31 @@ __global__ void __launch_bounds__(256, 3) gather_stats_kernel(
 
 // Q, K and V of one ba_select in ONE launch (one CTA per (side, block, batch*head),
 // sides laid out back to back in a 1-D grid): no inter-kernel drain between them.
-template <typename T, int D>
+template <typename T, int D, int NBLK>
 __global__ void __launch_bounds__(256, 3) gather_stats_multi_kernel(const GatherSides gs, int B) {
   int64_t c = blockIdx.x;
   int s = 0;
   while (s + 1 < gs.n && c >= gs.side[s].ctas) { c -= gs.side[s].ctas; ++s; }
   const GatherSide &sd = gs.side[s];
-  const int64_t nb = (sd.L + B - 1) / B;
-  gather_stats_body<T, D>(static_cast<const T *>(sd.x), sd.st[0], sd.st[1], sd.st[2], sd.heads, sd.L, B, sd.perm,
-                          sd.perm_id_out, static_cast<T *>(sd.xs), sd.mean, sd.var, c % nb, c / nb);
+  const int64_t ng = ((sd.L + B - 1) / B + NBLK - 1) / NBLK;  // block groups per (batch, head)
+  gather_stats_body<T, D, NBLK>(static_cast<const T *>(sd.x), sd.st[0], sd.st[1], sd.st[2], sd.heads, sd.L, B, sd.perm,
+                                sd.perm_id_out, static_cast<T *>(sd.xs), sd.mean, sd.var, c % ng, c / ng);
 }
 
 cudaError_t launch_gather_stats_multi(int dtype, int d, GatherSides gs, int B, cudaStream_t stream) {
+  const int nblk = B <= 64 ? 2 : 1;  // B = 64: two blocks per CTA (128 rows in flight)
   int64_t total = 0;
   for (int s = 0; s < gs.n; ++s) {
-    gs.side[s].ctas = ((gs.side[s].L + B - 1) / B) * gs.side[s].heads * gs.side[s].batch;
+    gs.side[s].ctas = (((gs.side[s].L + B - 1) / B + nblk - 1) / nblk) * gs.side[s].heads * gs.side[s].batch;
     total += gs.side[s].ctas;
   }
   if (total == 0) return cudaSuccess;
   // heads in gather_stats_body index one batch element's heads; bh runs over batch * heads
-#define BA_GM(T, D) gather_stats_multi_kernel<T, D><<<(unsigned)total, 256, 0, stream>>>(gs, B)
+#define BA_GM(T, D)                                                                     \
+  do {                                                                                  \
+    if (nblk == 2) gather_stats_multi_kernel<T, D, 2><<<(unsigned)total, 256, 0, stream>>>(gs, B); \
+    else gather_stats_multi_kernel<T, D, 1><<<(unsigned)total, 256, 0, stream>>>(gs, B);           \
+  } while (0)
   if (dtype == 0 && d == 128) BA_GM(__nv_bfloat16, 128);
   else if (dtype == 0 && d == 64) BA_GM(__nv_bfloat16, 64);
   else if (dtype == 1 && d == 128) BA_GM(float, 128);
