@@ -1,5 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider --timeout 300 -o timeout_method=thread -k "host or attention" 2>&1 | tail -2
-for cfg in C A; do
-timeout 300 python bench.py --config $cfg --no-cpu --no-dense > gpurun_out/e2e.json 2>/dev/null
-python -c "import json;d=json.load(open('gpurun_out/e2e.json'));print('$cfg value',round(d['value'],1),'e2e',d['e2e'])"
+python -m pytest tests/test_gpu_parity.py -q -x -k "host_api" 2>&1 | tail -1
+for c in A V M C; do
+python bench.py --config $c --steps 5 --warmup 3 --no-cpu --no-dense 2>/dev/null | tail -1 | python -c "import json,sys;d=json.loads(sys.stdin.read());print('$c value', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), d['clocks']['sm_mhz'])"
 done
