@@ -345,8 +345,15 @@ def run_ours(args):
         dist.barrier()
     clocks = sampler.stop() if sampler else None
     total_ms = t_start.elapsed_time(t_end)
-    sel_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
-    attn_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+    sel_each = [e[0].elapsed_time(e[1]) for e in ev]
+    attn_each = [e[1].elapsed_time(e[2]) for e in ev]
+    sel_ms = sum(sel_each) / args.steps
+    attn_ms = sum(attn_each) / args.steps
+
+    def pcts(xs):  # per-stage distribution over the timed steps (median, p10, p90)
+        ys = sorted(xs)
+        q = lambda f: ys[min(len(ys) - 1, max(0, int(round(f * (len(ys) - 1)))))]
+        return {"median": q(0.5), "p10": q(0.1), "p90": q(0.9)}
     ms_per_step = max_over_ranks(total_ms / args.steps, dev)
     flops_all = sum_over_ranks(flops_per_step, dev)
     value = flops_all / (ms_per_step * 1e-3) / 1e12
@@ -492,6 +499,7 @@ def run_ours(args):
             "gpu_launches": launches * args.steps,
             "clocks": clocks,
             "select_ms": sel_ms, "attn_ms": attn_ms, "select_share": sel_ms / (sel_ms + attn_ms),
+            "stage_ms": {"ba_select": pcts(sel_each), "ba_sparse_attn": pcts(attn_each)},
             "tokens_per_s": tokens / (ms_per_step * 1e-3),
             "flops_per_step_per_rank": flops_per_step,
         }
