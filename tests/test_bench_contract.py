@@ -29,3 +29,41 @@ def test_reference_arm_nonzero_rank_is_silent():
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1"],
                        capture_output=True, text=True, cwd=ROOT, timeout=300, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def _bench(args, env=None, timeout=600):
+    r = subprocess.run([sys.executable, "bench.py"] + args, capture_output=True, text=True, cwd=ROOT,
+                       timeout=timeout, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_bench_product_line_config_T():
+    """The product arm's JSON line on the small config (fp32 SIMT path): every
+    contract key, per-stage percentiles, a positive device-timed value and a
+    launch count from the library."""
+    d = _bench(["--config", "T", "--steps", "3", "--warmup", "3", "--no-cpu"])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks", "stage_ms"):
+        assert key in d, key
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["n_gpus"] == 1 and d["steps"] == 3
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert set(d["stage_ms"]) == {"ba_select", "ba_sparse_attn"}
+
+
+@pytest.mark.gpu
+def test_bench_unit_split_single_rank():
+    """--shard units on one rank (the uneven-split path of SURVEY 8(e): units
+    covering every head, ba_sparse_attn_units) produces the same work as the
+    default run."""
+    base = _bench(["--config", "T", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e", "--no-dense"])
+    d = _bench(["--config", "T", "--shard", "units", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e",
+                "--no-dense"])
+    assert d["scaling"] == "strong" and d["config"]["parallelism"].startswith("unit-parallel x1")
+    assert d["flops_per_step_per_rank"] == base["flops_per_step_per_rank"]
