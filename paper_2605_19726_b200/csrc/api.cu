@@ -293,6 +293,18 @@ AttnArgs make_attn(const Dims &D, const ba_params *pa) {
   return a;
 }
 
+// Attention over the permuted copies of a selection (contiguous [b, H, L, d]):
+// Q', K', V', kv_index / kv_count (row stride kappa) and pi_q; out / lse unset.
+AttnArgs make_attn_sorted(const Dims &D, const ba_params *pa, const ba_selection *sel) {
+  AttnArgs a = make_attn(D, pa);
+  a.q = sel->q_sorted; a.k = sel->k_sorted; a.v = sel->v_sorted;
+  a.qs[0] = D.hq * D.lq * D.d; a.qs[1] = D.lq * D.d; a.qs[2] = D.d;
+  a.ks[0] = D.hkv * D.lk * D.d; a.ks[1] = D.lk * D.d; a.ks[2] = D.d;
+  for (int i = 0; i < 3; ++i) a.vs[i] = a.ks[i];
+  a.kv_index = sel->kv_index; a.kv_count = sel->kv_count; a.kv_stride = D.kappa; a.perm_q = sel->perm_q;
+  return a;
+}
+
 // B = 128 kernel choice, BA_ATTN_K5 = "pp" (ping-pong pair, attn_sm100_pp.cu; the
 // default: +1.5-2% over 1cta on A and C), "2cta" (cluster pair,
 // attn_sm100_2cta.cu) or "1cta" (attn_sm100.cu).  The pair kernels walk the
@@ -349,15 +361,7 @@ ba_status run_sparse(const Dims &D, const ba_problem *prob, const ba_params *pa,
   BA_TRY(check_ptr("sel->v_sorted", sel->v_sorted));
   if (!sel->kv_index || !sel->kv_count || !sel->perm_q)
     return fail(BA_ERR_INVALID_ARGUMENT, "selection kv_index/kv_count/perm_q must be non-NULL");
-  AttnArgs a = make_attn(D, pa);
-  a.q = sel->q_sorted; a.k = sel->k_sorted; a.v = sel->v_sorted;
-  a.qs[0] = D.hq * D.lq * D.d; a.qs[1] = D.lq * D.d; a.qs[2] = D.d;
-  a.ks[0] = D.hkv * D.lk * D.d; a.ks[1] = D.lk * D.d; a.ks[2] = D.d;
-  for (int i = 0; i < 3; ++i) a.vs[i] = a.ks[i];
-  a.kv_index = sel->kv_index;
-  a.kv_count = sel->kv_count;
-  a.kv_stride = D.kappa;
-  a.perm_q = sel->perm_q;
+  AttnArgs a = make_attn_sorted(D, pa, sel);
   a.out = out;
   for (int i = 0; i < 3; ++i) a.os[i] = prob->o_stride[i];
   a.lse = lse;
@@ -507,14 +511,9 @@ ba_status ba_sparse_attn_peers(const ba_problem *prob, const ba_params *params, 
   if (!sel || !sel->q_sorted || !sel->k_sorted || !sel->v_sorted || !sel->kv_index || !sel->kv_count || !sel->perm_q)
     return fail(BA_ERR_INVALID_ARGUMENT, "ba_sparse_attn_peers reads the permuted copies, kv_index, kv_count, perm_q");
   BA_TRY(check_strides("o", prob->o_stride, D.esz));
-  AttnArgs a = make_attn(D, params);
+  AttnArgs a = make_attn_sorted(D, params, sel);
   if (!attn_sm100_supported(a) || use_pps(a) || use_2cta(a))
     return fail(BA_ERR_UNSUPPORTED, "peer stores need the bf16 tcgen05 pair / single-CTA kernels (d = 128)");
-  a.q = sel->q_sorted; a.k = sel->k_sorted; a.v = sel->v_sorted;
-  a.qs[0] = D.hq * D.lq * D.d; a.qs[1] = D.lq * D.d; a.qs[2] = D.d;
-  a.ks[0] = D.hkv * D.lk * D.d; a.ks[1] = D.lk * D.d; a.ks[2] = D.d;
-  for (int i = 0; i < 3; ++i) a.vs[i] = a.ks[i];
-  a.kv_index = sel->kv_index; a.kv_count = sel->kv_count; a.kv_stride = D.kappa; a.perm_q = sel->perm_q;
   a.out = out_peers[0];
   a.n_peers = n_peers;
   for (int p = 0; p < n_peers; ++p) a.out_peers[p] = out_peers[p];
@@ -550,14 +549,10 @@ ba_status ba_sparse_attn_units(const ba_problem *prob, const ba_params *params, 
   if (!sel || !sel->q_sorted || !sel->k_sorted || !sel->v_sorted || !sel->kv_index || !sel->kv_count || !sel->perm_q)
     return fail(BA_ERR_INVALID_ARGUMENT, "ba_sparse_attn_units reads the permuted copies, kv_index, kv_count, perm_q");
   BA_TRY(check_strides("o", prob->o_stride, D.esz));
-  AttnArgs base = make_attn(D, params);
+  AttnArgs base = make_attn_sorted(D, params, sel);
   if (n_out > 1 && (!attn_sm100_supported(base) || use_pps(base) || use_2cta(base)))
     return fail(BA_ERR_UNSUPPORTED, "peer stores need the bf16 tcgen05 pair / single-CTA kernels (d = 128)");
-  base.q = sel->q_sorted; base.k = sel->k_sorted; base.v = sel->v_sorted;
-  base.qs[0] = D.hq * D.lq * D.d; base.qs[1] = D.lq * D.d; base.qs[2] = D.d;
-  base.ks[0] = D.hkv * D.lk * D.d; base.ks[1] = D.lk * D.d; base.ks[2] = D.d;
-  for (int i = 0; i < 3; ++i) { base.vs[i] = base.ks[i]; base.os[i] = prob->o_stride[i]; }
-  base.kv_stride = D.kappa;
+  for (int i = 0; i < 3; ++i) base.os[i] = prob->o_stride[i];
   const int64_t grp = D.hq / D.hkv;
   int launches = 0;
   for (int64_t u = unit_begin; u < unit_end;) {
@@ -831,12 +826,9 @@ ba_status ba_block_mass(const ba_problem *prob, const ba_params *params, const b
   float *lse = at<float>(workspace, 0);
   void *o_scratch = at<void>(workspace, align_up(4ull * D.b * D.hq * D.lq));
   // 1. dense attention over the sorted copies: the row normaliser (LSE, sorted order)
-  AttnArgs a = make_attn(D, params);
-  a.q = sel->q_sorted; a.k = sel->k_sorted; a.v = sel->v_sorted;
-  a.qs[0] = D.hq * D.lq * D.d; a.qs[1] = D.lq * D.d; a.qs[2] = D.d;
-  a.ks[0] = D.hkv * D.lk * D.d; a.ks[1] = D.lk * D.d; a.ks[2] = D.d;
-  for (int i = 0; i < 3; ++i) { a.vs[i] = a.ks[i]; a.os[i] = a.qs[i]; }
-  a.kv_index = nullptr; a.kv_count = nullptr; a.kv_stride = D.nk; a.perm_q = nullptr;
+  AttnArgs a = make_attn_sorted(D, params, sel);
+  for (int i = 0; i < 3; ++i) a.os[i] = a.qs[i];
+  a.kv_index = nullptr; a.kv_count = nullptr; a.kv_stride = D.nk; a.perm_q = nullptr;  // dense, sorted order
   a.out = o_scratch; a.lse = lse;
   BA_TRY(run_attn(a, stream));
   // 2. S again, exp(S*scale - lse) reduced per (query block, key block)
