@@ -88,6 +88,26 @@ def test_selection_deterministic(ba):
         assert torch.equal(getattr(s1, f), getattr(s2, f)), f
 
 
+@pytest.mark.parametrize("cfg,L,hq,hkv,B", [("C", 4096 + 50, 8, 2, 128), ("M", 4096 + 17, 4, 4, 64), ("T", 1024, 1, 1, 64)])
+def test_attention_deterministic(ba, cfg, L, hq, hkv, B):
+    """SURVEY 8(e) correctness premise: the whole path is deterministic (no
+    atomics in any reduction that feeds O), so repeated calls — and therefore
+    every rank of a multi-GPU split — reproduce O and LSE bit for bit."""
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv)
+    outs = []
+    for _ in range(3):
+        ctx = ba.Context(q, k, v, B, 0.5)
+        ctx.select(q, k, v)
+        o = torch.empty_like(q)
+        lse = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+        ctx.sparse_attn(o, lse)
+        outs.append((o, lse))
+    torch.cuda.synchronize()
+    for o, lse in outs[1:]:
+        assert torch.equal(o, outs[0][0]) and torch.equal(lse, outs[0][1])
+
+
 # ---------------------------------------------------------------- attention (P5, P6)
 def test_attention_fp32_T(ba):
     """Config T end to end: output within 1e-5 of the fp64 oracle."""
