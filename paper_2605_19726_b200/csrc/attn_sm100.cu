@@ -408,14 +408,17 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       if (lane == 0 && qd == 0) TR(6 + 5 * hf, j);
       float pmax = -INFINITY;
       if (mine) {
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        static_assert(HC % 16 == 0, "8 max chains");
+        float m8[8];  // 8 independent FMNMX3 chains: latency, not issue, bounds the lone warp here
 #pragma unroll
-        for (int i = 0; i < HC; i += 8) {
+        for (int u = 0; u < 8; ++u) m8[u] = fmaxf(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            m4[u] = fmax3(m4[u], __uint_as_float(sr[i + 2 * u]), __uint_as_float(sr[i + 2 * u + 1]));
+        for (int i = 16; i < HC; i += 16) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            m8[u] = fmax3(m8[u], __uint_as_float(sr[i + 2 * u]), __uint_as_float(sr[i + 2 * u + 1]));
         }
-        pmax = fmaxf(fmax3(m4[0], m4[1], m4[2]), m4[3]);
+        pmax = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
       }
       // swap partial maxima with the other half of the row (red is double-buffered by j;
       // every tile passes the barrier, selected or not, so the buffer reuse stays safe)
