@@ -157,6 +157,22 @@ def test_attention_bf16(ba, cfg, L, hq, hkv, dens):
     assert torch.isfinite(lse).all()
 
 
+@pytest.mark.parametrize("B,L,hq,hkv", [(128, 2048 + 45, 4, 2), (64, 1024 + 9, 2, 2)])
+def test_head_dim_64_bf16(ba, B, L, hq, hkv):
+    """head_dim = 64 in bf16 (an ABI combination off the tcgen05 kernels): the
+    selection matches the oracle's and the attention matches the oracle run
+    with the GPU's selection."""
+    w = CONFIGS["A"].with_(head_dim=64, block_size=B)
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv)
+    ctx, sel = _run_select(ba, q, k, v, B, 0.5)
+    out = torch.empty_like(q)
+    ctx.sparse_attn(out)
+    torch.cuda.synchronize()
+    check_selection(sel, oracle_select_all(q, k, B, 0.5, 1.0, "qk", "diag"))
+    err = max_abs_err(out, oracle_output_with_gpu_selection(q, k, v, sel, B))
+    assert err <= TOL[torch.bfloat16], err
+
+
 @pytest.mark.parametrize("L,dens", [(2048 + 33, 0.5), (64 * 31 + 5, 0.3), (64 * 7, 1.0), (100, 0.5)])
 def test_attention_bf16_B64(ba, L, dens):
     """B = 64 (dual tiles: two 64-key blocks per 128-key MMA tile), ragged last
