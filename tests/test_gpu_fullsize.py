@@ -127,3 +127,34 @@ def test_max_length_one_million_tokens(ba):
     for g in blocks:
         rows = pq[g * 128:(g + 1) * 128]
         assert np.abs(gout[rows] - Os[g * 128:(g + 1) * 128]).max() <= TOL[q.dtype]
+
+
+@pytest.mark.parametrize("cfg,world", [("M", 8), ("C", 3)])
+def test_unit_split_full_size_bitwise(ba, cfg, world):
+    """SURVEY 8(e) at full size: config M's 28 heads on 8 simulated ranks (and C's
+    8 GQA groups on 3, splitting a group) — each rank selects over the heads its
+    (head, q-block) units touch and runs ba_sparse_attn_units; the union of the
+    ranks' rows equals the 1-GPU output bit for bit."""
+    from paper_2605_19726_b200.dist import unit_heads, unit_range
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cuda")
+    ref = torch.empty_like(q)
+    ctx = ba.Context(q, k, v, w.block_size, w.density)
+    ctx.select(q, k, v)
+    ctx.sparse_attn(ref)
+    nq = ctx.sel.n_q
+    del ctx
+    out = torch.full_like(q, float("nan"))
+    sizes = []
+    for r in range(world):
+        u0, u1 = unit_range(w.heads_q, nq, world, r)
+        sizes.append(u1 - u0)
+        q0, q1, k0, k1 = unit_heads(u0, u1, nq, w.heads_q, w.heads_kv)
+        qs, ks, vs = q[:, q0:q1].contiguous(), k[:, k0:k1].contiguous(), v[:, k0:k1].contiguous()
+        c = ba.Context(qs, ks, vs, w.block_size, w.density, out=out[:, q0:q1])
+        c.select(qs, ks, vs)
+        c.sparse_attn_units(u0 - q0 * nq, u1 - q0 * nq, [out[:, q0:q1]])
+        del c, qs, ks, vs
+    torch.cuda.synchronize()
+    assert max(sizes) - min(sizes) <= 2
+    assert torch.equal(out, ref)
