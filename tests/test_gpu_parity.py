@@ -581,3 +581,51 @@ def test_sparse_attn_units_batch_and_peers(ba):
         assert torch.equal(o, ref)
     with pytest.raises(ba.BaError):
         ctx.sparse_attn_units(0, n + 1, outs[:1])
+
+
+def test_fused_head_gather_symmetric_memory(tmp_path):
+    """The fused output collective end to end on one rank under torchrun: NCCL
+    process group, a symmetric-memory full O (torch symm_mem rendezvous), the
+    attention epilogue storing through the peer pointers (ba_sparse_attn_peers,
+    and ba_sparse_attn_units for a unit split), then the symmetric barrier —
+    equal to ba_sparse_attn bit for bit."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "fused.py"
+    script.write_text(f"""
+import sys; sys.path.insert(0, {root!r}); sys.path.insert(0, {os.path.dirname(os.path.abspath(__file__))!r})
+import torch, torch.distributed as dist
+import paper_2605_19726_b200.baatt as ba
+from paper_2605_19726_b200.dist import FusedHeadGather
+from synth import CONFIGS, make_qkv
+dev = torch.device("cuda", 0)
+torch.cuda.set_device(dev)
+dist.init_process_group("nccl", device_id=dev)
+w = CONFIGS["C"]
+q, k, v = make_qkv(w, device=dev, seq_len=2048 + 64, heads_q=8, heads_kv=2)
+ref = torch.empty_like(q)
+c0 = ba.Context(q, k, v, 128, 0.5)
+c0.select(q, k, v)
+c0.sparse_attn(ref)
+f = FusedHeadGather(tuple(q.shape), q.dtype, dev, 0)
+f.full.fill_(float("nan"))
+ctx = ba.Context(q, k, v, 128, 0.5, out=f.full)
+ctx.select(q, k, v)
+ctx.sparse_attn_peers(f.peer_ptrs)
+f.barrier()
+torch.cuda.synchronize()
+ok1 = torch.equal(f.full, ref)
+f.full.fill_(float("nan"))
+n = 8 * ctx.sel.n_q
+ctx.sparse_attn_units(0, n // 3, f.peer_ptrs)
+ctx.sparse_attn_units(n // 3, n, f.peer_ptrs)
+f.barrier()
+torch.cuda.synchronize()
+ok2 = torch.equal(f.full, ref)
+dist.destroy_process_group()
+print("RESULT", ok1, ok2)
+""")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", "29561", str(script)],
+                       capture_output=True, text=True, timeout=300, cwd=root)
+    assert "RESULT True True" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
