@@ -194,6 +194,16 @@ def oracle_sample(w, q, k, v, density, n_blocks, seed=0):
     return fl, secs, desc
 
 
+def oracle_dense_sample(w, q, k, v, n_rows):
+    """The oracle's dense attention for the first `n_rows` query rows
+    of one head against every key, timed as the CPU dense reference (SURVEY
+    8(d4)).  Returns (flops, seconds)."""
+    import oracle as O
+    t0 = time.perf_counter()
+    O.dense_attention(q[:n_rows], k, v, 1.0 / math.sqrt(w.head_dim), row_block=128)
+    return 4.0 * n_rows * k.shape[0] * w.head_dim, time.perf_counter() - t0
+
+
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args):
     import torch
@@ -455,6 +465,12 @@ def run_ours(args):
         n_blocks = 8 if w.seq_len >= 65536 else 16
         fl, secs, desc = oracle_sample(w, qn, kn, vn, density, n_blocks)
         cpu = {"value": fl / secs / 1e12, "unit": "TFLOP/s", "cores": cpu_cores(), "kind": "oracle", "sample": desc}
+        n_rows = min(qn.shape[0], 4 * w.block_size)
+        dfl, dsecs = oracle_dense_sample(w, qn, kn, vn, n_rows)
+        cpu["dense"] = {"value": dfl / dsecs / 1e12, "unit": "TFLOP/s",
+                        "sample": f"oracle dense attention of {n_rows} query rows of 1 head against all {kn.shape[0]} "
+                                  f"keys ({dsecs:.2f}s)",
+                        "ms_per_step_extrapolated": dsecs * (q.shape[1] * q.shape[2] / n_rows) * 1e3}
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
