@@ -289,22 +289,24 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         tc_fence_after();
       };
       auto issue_s = [&](int x, int u) {  // S_x = Q_x K_u^T into S_x's TMEM columns
-        const uint32_t sq = base + SMEM_Q + x * TILE, sk = slot_addr(2 * u);
+        // descriptors built once per tile; the K-step offsets are added to the start-address
+        // field (addr >> 4, 14 bits: every smem address here is < 256 KB, so no carry out)
+        const uint64_t dq = make_desc(base + SMEM_Q + x * TILE, 16, 1024), dk = make_desc(slot_addr(2 * u), 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * BOX + (kk & 3) * 32;
-          mma_ss(tmem + s_col(x), make_desc(sq + off, 16, 1024), make_desc(sk + off, 16, 1024), IDESC_S, kk > 0 ? 1u : 0u);
+          const uint64_t off = ((kk >> 2) * BOX + (kk & 3) * 32) >> 4;
+          mma_ss(tmem + s_col(x), dq + off, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
         }
         mma_commit(&bars.s_full[x]);
       };
       // O_x += P_x V_u, P_x read from TMEM, in two halves of 64 keys: the first half is issued
       // as soon as the softmax has stored P for keys 0-63 (p_half), overlapping its second half
       auto issue_pv = [&](int x, int u, int h) {
-        const uint32_t sv = slot_addr(2 * u + 1);
+        const uint64_t dv = make_desc(slot_addr(2 * u + 1), BOX, 1024);
         constexpr int KPP = BN / 16 / kPSplit;  // 16-key MMA steps per part
 #pragma unroll
         for (int kk = KPP * h; kk < KPP * h + KPP; ++kk)
-          mma_ts(tmem + O_COL0 + 128 * x, tmem + s_col(x) + kk * 8, make_desc(sv + kk * 2048, BOX, 1024), IDESC_O,
+          mma_ts(tmem + O_COL0 + 128 * x, tmem + s_col(x) + kk * 8, dv + (uint64_t)((kk * 2048) >> 4), IDESC_O,
                  (u > 0 || kk > 0) ? 1u : 0u);
       };
       wait_full(0);
