@@ -21,7 +21,7 @@ Pin status (see tests/test_oracle_pins.py):
   norm_key, norm_rank, apply/unapply_permutation, make_grid, block_stats,
   block_logits, compensation_diag, compensation_exact, softmax_rows,
   kappa_from_density, topk_mask, topp_mask, select_head, block_sparse_attention_head,
-  dense_attention, oracle_block_mass, deviation_bound, lemma_check,
+  dense_attention, oracle_block_mass, deviation_bound, max_logit_deviation, lemma_check,
   ba_attention — all pinned (closed forms, worked examples, brute force,
   invariants).  Nothing here is "parity unpinned".
 """
@@ -375,6 +375,25 @@ def deviation_bound(Xq, Xk, B: int):
     RQ, MQ = rm(Xq)
     RK, MK = rm(Xk)
     return (np.outer(RQ, MK) + np.outer(MQ, RK) + np.outer(RQ, RK)) / math.sqrt(d)
+
+
+def max_logit_deviation(Xq, Xk, B: int):
+    """max_{i in I(g_q), j in J(g_k)} |l_hat_ij - l_{g_q,g_k}| per block pair, with
+    l_hat_ij = Q_i . K_j / sqrt(d) (the token logit) and l = Qbar . Kbar / sqrt(d)
+    (Eq. block-logit): the "observed maximum logit deviation" that Fig. 2
+     plots against U (Eq. logit-deviation).  Brute force over
+    every token pair of every block pair."""
+    Xq, Xk = _f64(Xq), _f64(Xk)
+    d = Xq.shape[1]
+    gq, gk = make_grid(Xq.shape[0], B), make_grid(Xk.shape[0], B)
+    out = np.empty((len(gq), len(gk)))
+    for a, (s, e) in enumerate(gq):
+        qbar = Xq[s:e].mean(axis=0)
+        for b, (u, v) in enumerate(gk):
+            kbar = Xk[u:v].mean(axis=0)
+            tok = Xq[s:e] @ Xk[u:v].T / math.sqrt(d)
+            out[a, b] = np.abs(tok - (qbar @ kbar) / math.sqrt(d)).max()
+    return out
 
 
 def lemma_check(u, v):

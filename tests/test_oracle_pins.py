@@ -311,6 +311,35 @@ def test_bound_worked(golden):
     assert np.abs(O.deviation_bound(X, X, 4)).max() == 0
 
 
+def test_max_logit_deviation_pins():
+    """max_logit_deviation (the Fig. 2 ordinate) against: a worked
+    example (d = 2: Q block {(1,0),(-1,0)}, K block {(2,0),(0,0)}: Qbar = 0, so l = 0
+    and the extreme token logits are +-2/sqrt2 -> sqrt2; U = (1*2 + 1*1 + 1*1)/sqrt2
+    = 2 sqrt2), the three-term decomposition of Eq. logit-deviation
+    evaluated independently, U as an upper bound (Eq. logits-bound),
+    constant blocks and B = 1 (tokens are their own blocks) -> 0."""
+    X = np.array([[1.0, 0.0], [-1.0, 0.0]])
+    Y = np.array([[2.0, 0.0], [0.0, 0.0]])
+    assert abs(O.max_logit_deviation(X, Y, 2)[0, 0] - math.sqrt(2)) <= 1e-15
+    assert abs(O.deviation_bound(X, Y, 2)[0, 0] - 2 * math.sqrt(2)) <= 1e-15
+    for _ in range(5):
+        d, B = 8, 8
+        X = RNG.standard_normal((40, d)) * np.exp(RNG.normal(size=(40, 1)))
+        Y = RNG.standard_normal((29, d)) * np.exp(RNG.normal(size=(29, 1)))
+        dev = O.max_logit_deviation(X, Y, B)
+        U = O.deviation_bound(X, Y, B)
+        assert (dev <= U + 1e-12).all()
+        for a, (s, e) in enumerate(O.make_grid(40, B)):
+            for b, (u, v) in enumerate(O.make_grid(29, B)):
+                qb, kb = X[s:e].mean(0), Y[u:v].mean(0)
+                dq, dk = X[s:e] - qb, Y[u:v] - kb
+                three = ((dq @ kb)[:, None] + (qb @ dk.T)[None, :] + dq @ dk.T) / math.sqrt(d)
+                assert abs(np.abs(three).max() - dev[a, b]) <= 1e-12 * (1 + dev[a, b])
+    C = np.repeat(RNG.standard_normal((3, 4)), 4, axis=0)
+    assert np.abs(O.max_logit_deviation(C, C, 4)).max() <= 1e-14
+    assert np.abs(O.max_logit_deviation(X, Y, 1)).max() <= 1e-12
+
+
 # ---------------------------------------------------------------- budget and top-k
 def test_kappa(golden):
     for rho, nk, exp in golden["kappa_configs"]["cases"]:
