@@ -36,8 +36,10 @@
  *    nothing is enqueued and ba_last_error() names the offending field.
  *  - No C++ exception crosses the ABI.  The library is thread-safe for
  *    concurrent calls on different streams (no global mutable state other
- *    than idempotent per-device kernel attributes and the thread-local error
- *    string).
+ *    than idempotent per-device kernel attributes, the thread-local error
+ *    string, ba_attention_host's two cached copy streams per device and the
+ *    device-error latch of ba_check_errors: 8 bytes of mapped pinned host
+ *    memory, allocated once per process).
  *  - Tensor layout: element (b, h, t, c) of q/k/v/out lives at
  *    base + b*stride[0] + h*stride[1] + t*stride[2] + c (element units; the
  *    feature stride is 1).  Strides and base pointers must be 16-byte aligned
@@ -69,7 +71,9 @@ typedef enum {
   BA_ERR_UNSUPPORTED = 3,        /* valid but not implemented (head_dim, block_size, dtype combo) */
   BA_ERR_WORKSPACE_TOO_SMALL = 4,
   BA_ERR_CUDA = 5,               /* a CUDA runtime call or launch failed */
-  BA_ERR_EMPTY_MASK_ROW = 6      /* kappa < 1 (every mask row must be non-empty) */
+  BA_ERR_EMPTY_MASK_ROW = 6      /* a query block with kv_count < 1 reached the attention (every mask row
+                                    must be non-empty); detected on the device, reported by
+                                    ba_check_errors / the next attention call (see below) */
 } ba_status;
 
 typedef enum { BA_DTYPE_BF16 = 0, BA_DTYPE_FP32 = 1 } ba_dtype;
@@ -157,7 +161,9 @@ ba_status ba_selection_sizes(const ba_problem *prob, const ba_params *params,
                              int64_t *kappa, int64_t *n_q, int64_t *n_k);
 
 /* Scratch bytes needed by ba_select (sort buffers, histograms, stats and the
- * fp64 score map when not supplied).  0 on an invalid problem. */
+ * fp64 score map when not supplied).  0 on an invalid problem.  ba_select
+ * supports N_k <= 28672 key blocks (its top-kappa row buffer lives in shared
+ * memory): larger problems return BA_ERR_UNSUPPORTED before any launch. */
 size_t ba_select_workspace_size(const ba_problem *prob, const ba_params *params);
 
 /* Scratch bytes needed by ba_attention: ba_select's scratch plus every
@@ -176,7 +182,23 @@ ba_status ba_select(const ba_problem *prob, const ba_params *params,
  * kv_count, perm_q (a caller may inject its own selection: kv_index rows must
  * be ascending, unique, in [0, N_k), with kv_count >= 1).  out: original
  * token order, ba_problem o_stride layout.  lse: optional [b, H_q, L_q] fp32
- * natural-log log-sum-exp of the scaled logits per query row, original order. */
+ * natural-log log-sum-exp of the scaled logits per query row, original order.
+ *
+ * Injected selections are checked ON THE DEVICE (checking them on the host
+ * would need a synchronising copy): a query block whose kv_count < 1 violates
+ * the non-empty-row precondition — its rows are written as O = 0,
+ * LSE = -inf (deterministic, never unwritten accumulator memory) and
+ * BA_ERR_EMPTY_MASK_ROW is latched; a kv_index entry outside [0, N_k) is
+ * skipped and BA_ERR_INVALID_ARGUMENT latched.  A latched error is returned
+ * (and cleared) by ba_check_errors, or by the next ba_sparse_attn* /
+ * ba_attention / ba_dense_attn call on any thread once the faulting kernel
+ * has finished — like CUDA's asynchronous errors.  The latch is one pair of
+ * words of mapped pinned host memory per process, allocated on first use.
+ *
+ * bf16 with head_dim 128 always runs a tcgen05 kernel; problems those
+ * kernels cannot take (N_k > 32768 key blocks) return BA_ERR_UNSUPPORTED —
+ * never a silent SIMT fallback.  bf16 head_dim 64 and every fp32 problem run
+ * the SIMT kernel (ba_attention_kernel_name says which). */
 ba_status ba_sparse_attn(const ba_problem *prob, const ba_params *params,
                          const ba_selection *sel, void *out, float *lse,
                          cudaStream_t stream);
@@ -285,12 +307,37 @@ ba_status ba_block_mass(const ba_problem *prob, const ba_params *params, const b
                         float *m_hat, float *captured, void *workspace, size_t workspace_bytes,
                         cudaStream_t stream);
 
+/* NEXT-3 fidelity diagnostic: the bound of Eq. logits-bound
+ *   U[g_q, g_k] = (R^Q M^K + M^Q R^K + R^Q R^K) / sqrt(d),
+ *   R = max_{i in block} ||x_i - xbar||_2, M = max_{i in block} ||x_i||_2,
+ * and the observed maximum logit deviation it bounds (Fig. 2, P:386-392;
+ * Eq. logit-deviation)
+ *   max_dev[g_q, g_k] = max_{i in I(g_q), j in J(g_k)} |Q'_i.K'_j/sqrt(d) - Qbar.Kbar/sqrt(d)|
+ * per block pair of the norm-sorted block space of a selection (the paper's
+ * "red group").  Reads sel->q_sorted, k_sorted and the fp64 block means
+ * sel->q_mean, k_mean (pass those buffers to ba_select).  bound_u, max_dev:
+ * [b, H_q, N_q, N_k] fp64 (either may be NULL).  R and M are fp64 against the
+ * fp64 means; the token logits come from a dense S = Q'K'^T pass on the
+ * tensor cores (bf16 inputs, fp32 accumulation: |error| <= d*2^-24 * M^Q M^K),
+ * the block logit from an fp64 DMMA.  bf16, head_dim 128, block_size 128
+ * (else BA_ERR_UNSUPPORTED).  workspace >= ba_deviation_workspace_size. */
+size_t ba_deviation_workspace_size(const ba_problem *prob, const ba_params *params);
+ba_status ba_deviation(const ba_problem *prob, const ba_params *params, const ba_selection *sel,
+                       double *bound_u, double *max_dev, void *workspace, size_t workspace_bytes,
+                       cudaStream_t stream);
+
 /* Name of the attention kernel ba_sparse_attn / ba_attention / ba_dense_attn
  * run for this problem: "attn_sm100_tcgen05" (bf16, d = 128, B in {64, 128}:
  * tcgen05 tensor cores, TMA, TMEM; B = 64 pairs two query blocks per 128-row
  * tile) or "attn_simt" (fp32 inputs, and bf16 d = 64).  "" on an invalid
  * problem. */
 const char *ba_attention_kernel_name(const ba_problem *prob, const ba_params *params);
+
+/* Synchronises `stream`, then returns (and clears) an error the attention
+ * kernels latched on the device (BA_ERR_EMPTY_MASK_ROW: a query block with
+ * kv_count < 1; BA_ERR_INVALID_ARGUMENT: a kv_index entry outside
+ * [0, N_k)), or BA_ERR_CUDA if the synchronisation failed; BA_OK otherwise. */
+ba_status ba_check_errors(cudaStream_t stream);
 
 /* Number of kernel launches the last successful call on this thread enqueued. */
 int ba_last_launch_count(void);

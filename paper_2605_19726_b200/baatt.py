@@ -86,6 +86,10 @@ def load() -> ctypes.CDLL:
     lib.ba_block_mass_workspace_size.restype = sz
     lib.ba_block_mass.argtypes = [P, PA, S, vp, vp, vp, sz, st]
     lib.ba_block_mass.restype = ctypes.c_int
+    lib.ba_deviation_workspace_size.argtypes = [P, PA]
+    lib.ba_deviation_workspace_size.restype = sz
+    lib.ba_deviation.argtypes = [P, PA, S, vp, vp, vp, sz, st]
+    lib.ba_deviation.restype = ctypes.c_int
     lib.ba_sparse_attn_peers.argtypes = [P, PA, S, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, vp, st]
     lib.ba_sparse_attn_peers.restype = ctypes.c_int
     lib.ba_sparse_attn_units.argtypes = [P, PA, S, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p),
@@ -100,6 +104,8 @@ def load() -> ctypes.CDLL:
     lib.ba_attention_host.argtypes = [P, PA, vp, vp, vp, vp, vp, sz, st]
     lib.ba_attention_host.restype = ctypes.c_int
     lib.ba_last_launch_count.restype = ctypes.c_int
+    lib.ba_check_errors.argtypes = [st]
+    lib.ba_check_errors.restype = ctypes.c_int
     lib.ba_attention_kernel_name.argtypes = [P, PA]
     lib.ba_attention_kernel_name.restype = ctypes.c_char_p
     lib.ba_status_string.argtypes = [ctypes.c_int]
@@ -113,7 +119,8 @@ EXPORTED = ["ba_abi_version", "ba_selection_sizes", "ba_select_workspace_size", 
             "ba_select", "ba_sparse_attn", "ba_sparse_attn_gather", "ba_sparse_attn_peers", "ba_sparse_attn_units",
             "ba_zero_copy_supported",
             "ba_attention", "ba_dense_attn", "ba_block_mass_workspace_size", "ba_block_mass",
-            "ba_attention_host_workspace_size", "ba_attention_host", "ba_last_launch_count",
+            "ba_deviation_workspace_size", "ba_deviation",
+            "ba_attention_host_workspace_size", "ba_attention_host", "ba_last_launch_count", "ba_check_errors",
             "ba_attention_kernel_name",
             "ba_status_string", "ba_last_error"]
 
@@ -143,6 +150,13 @@ def q_gather_supported(q, k, v, block_size=128) -> bool:
 
 def last_launch_count() -> int:
     return load().ba_last_launch_count()
+
+
+def ba_check_errors(stream=None) -> None:
+    """Synchronise the stream and raise the error the attention kernels latched on
+    the device, if any (BA_ERR_EMPTY_MASK_ROW for a query block with kv_count < 1,
+    S:393; BA_ERR_INVALID_ARGUMENT for a kv_index entry outside [0, N_k))."""
+    _check(load().ba_check_errors(_stream(stream)))
 
 
 def _stream(stream=None) -> ctypes.c_void_p:
@@ -190,6 +204,10 @@ def selection_sizes(prob: Problem, params: Params):
     _check(load().ba_selection_sizes(ctypes.byref(prob), ctypes.byref(params), ctypes.byref(kap),
                                      ctypes.byref(nq), ctypes.byref(nk)))
     return kap.value, nq.value, nk.value
+
+
+def _layout(t: torch.Tensor):
+    return (tuple(t.shape), tuple(t.stride()), t.dtype, str(t.device))
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
@@ -286,12 +304,45 @@ class Context:
                           "(see ba_sparse_attn_gather in include/ba_attn.h)")
         self.sel = alloc_selection(q, k, self.prob, self.params, diagnostics, zero_copy)
         self.sel_c = self.sel.to_c()
+        self._layout = tuple(_layout(t) for t in (q, k, v))
         self.qkv = (q, k, v)
 
+    def _check_inputs(self, q, k, v):
+        got = tuple(_layout(t) for t in (q, k, v))
+        if got != self._layout:
+            raise BaError(f"BA_ERR_SHAPE_MISMATCH: q/k/v (shape, stride, dtype, device) {got} differ from the "
+                          f"problem this Context was built for {self._layout}")
+
+    def _check_out(self, out, lse=None):
+        """out must have the o_stride layout baked into the problem (a mismatch would
+        be written with the wrong strides) and the q shape; lse is [b, Hq, Lq] fp32."""
+        q = self.qkv[0]
+        os = tuple(self.prob.o_stride)
+        # strides of size-1 dims are never used for addressing, so they need not match
+        same = all(out.shape[i] == 1 or out.stride(i) == os[i] for i in range(3)) if out.dim() == 4 else False
+        if tuple(out.shape) != tuple(q.shape) or out.dtype != q.dtype or out.stride(3) != 1 or not same:
+            raise BaError(f"BA_ERR_SHAPE_MISMATCH: out {tuple(out.shape)} strides {tuple(out.stride())} do not match "
+                          f"the problem's [b, Hq, Lq, d] {tuple(q.shape)} with o_stride {os} (pass out= at construction)")
+        if lse is not None and (tuple(lse.shape) != tuple(q.shape[:3]) or lse.dtype != torch.float32
+                                or not lse.is_contiguous()):
+            raise BaError("BA_ERR_SHAPE_MISMATCH: lse must be a contiguous fp32 [b, Hq, Lq] tensor")
+
+    def _check_sel(self, sel: "Selection"):
+        """An injected selection must have this problem's kappa / N_q / N_k: the C side
+        strides kv_index rows by kappa(density) of these params."""
+        kap, nq, nk = selection_sizes(self.prob, self.params)
+        if (sel.kappa, sel.n_q, sel.n_k) != (kap, nq, nk) or tuple(sel.kv_index.shape[2:]) != (nq, kap):
+            raise BaError(f"BA_ERR_SHAPE_MISMATCH: selection (kappa, N_q, N_k) = {(sel.kappa, sel.n_q, sel.n_k)} "
+                          f"but this Context's params give {(kap, nq, nk)}")
+
     def select(self, q, k, v, stream=None) -> Selection:
+        """Alg. 1 steps 1-10 on (q, k, v), which must have the layout the Context was
+        built for; the zero-copy attention then reads these tensors."""
+        self._check_inputs(q, k, v)
         _check(load().ba_select(ctypes.byref(self.prob), ctypes.byref(self.params), _ptr(q), _ptr(k), _ptr(v),
                                 ctypes.byref(self.sel_c), _ptr(self.ws_select), self.ws_select.numel(),
                                 _stream(stream)))
+        self.qkv = (q, k, v)
         return self.sel
 
     def block_mass(self, captured: bool = True, stream=None):
@@ -307,6 +358,22 @@ class Context:
                                  _ptr(m_hat), _ptr(cap), _ptr(ws), ws.numel(), _stream(stream)))
         return m_hat, cap
 
+    def deviation(self, stream=None):
+        """NEXT-3: (U, max_dev) [b, Hq, Nq, Nk] fp64 of the last selection (ba_deviation):
+        the bound of Eq. logits-bound and the observed max |l_hat - l| per block pair
+        (Fig. 2).  Needs a Context built with diagnostics=True."""
+        lib = load()
+        if self.sel.q_mean is None:
+            raise BaError("BA_ERR_INVALID_ARGUMENT: ba_deviation needs the block means (Context(diagnostics=True))")
+        q = self.qkv[0]
+        b, hq = q.shape[0], q.shape[1]
+        U = torch.empty(b, hq, self.sel.n_q, self.sel.n_k, dtype=torch.float64, device=q.device)
+        dev = torch.empty_like(U)
+        ws = _workspace(lib.ba_deviation_workspace_size(ctypes.byref(self.prob), ctypes.byref(self.params)), q.device)
+        _check(lib.ba_deviation(ctypes.byref(self.prob), ctypes.byref(self.params), ctypes.byref(self.sel_c), _ptr(U),
+                                _ptr(dev), _ptr(ws), ws.numel(), _stream(stream)))
+        return U, dev
+
     def sparse_attn_peers(self, peer_ptrs, lse=None, stream=None):
         """Fused output collective: store every output row to each of the device
         pointers in peer_ptrs (ba_sparse_attn_peers); strides are those of `out`
@@ -320,12 +387,21 @@ class Context:
         (ba_sparse_attn_units): rows stored at their original positions in every
         output of `outs` (tensors or device pointers; strides those of `out` given
         at construction)."""
+        for o in outs:
+            if isinstance(o, torch.Tensor):
+                self._check_out(o)
+        if lse is not None and (tuple(lse.shape) != tuple(self.qkv[0].shape[:3]) or lse.dtype != torch.float32
+                                or not lse.is_contiguous()):
+            raise BaError("BA_ERR_SHAPE_MISMATCH: lse must be a contiguous fp32 [b, Hq, Lq] tensor")
         ptrs = [o.data_ptr() if isinstance(o, torch.Tensor) else int(o) for o in outs]
         arr = (ctypes.c_void_p * len(ptrs))(*[ctypes.c_void_p(p) for p in ptrs])
         _check(load().ba_sparse_attn_units(ctypes.byref(self.prob), ctypes.byref(self.params), ctypes.byref(self.sel_c),
                                            int(unit_begin), int(unit_end), arr, len(ptrs), _ptr(lse), _stream(stream)))
 
     def sparse_attn(self, out, lse=None, sel: Optional[Selection] = None, stream=None):
+        self._check_out(out, lse)
+        if sel is not None:
+            self._check_sel(sel)
         sc = self.sel_c if sel is None else sel.to_c()
         if self.zero_copy:
             q, k, v = self.qkv
@@ -343,13 +419,21 @@ def ba_select(q, k, v, block_size=128, density=0.5, beta=1.0, sort="qk", comp="d
     return ctx.select(q, k, v, stream)
 
 
-def ba_sparse_attn(q, k, v, sel: Selection, block_size=128, density=0.5, softmax_scale=0.0,
+def ba_sparse_attn(q, k, v, sel: Selection, block_size=128, density=None, softmax_scale=0.0,
                    out=None, lse=None, stream=None):
-    """Attention half only, with a given (possibly injected) selection."""
+    """Attention half only, with a given (possibly injected) selection.  density:
+    None = the selection's own kappa / N_k (the C side strides kv_index rows by
+    kappa(density)); an explicit density must give the selection's kappa."""
     if out is None:
         out = torch.empty_like(q)
     prob = make_problem(q, k, v, out, block_size)
+    if density is None:
+        density = sel.kappa / sel.n_k
     params = make_params(density=density, softmax_scale=softmax_scale)
+    kap, nq, nk = selection_sizes(prob, params)
+    if (kap, nq, nk) != (sel.kappa, sel.n_q, sel.n_k) or tuple(sel.kv_index.shape[2:]) != (nq, kap):
+        raise BaError(f"BA_ERR_SHAPE_MISMATCH: selection (kappa, N_q, N_k) = {(sel.kappa, sel.n_q, sel.n_k)} but "
+                      f"density={density}, block_size={block_size} give {(kap, nq, nk)}")
     sc = sel.to_c()
     _check(load().ba_sparse_attn(ctypes.byref(prob), ctypes.byref(params), ctypes.byref(sc), _ptr(out),
                                  _ptr(lse), _stream(stream)))

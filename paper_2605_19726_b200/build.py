@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbaatt.so")
-SOURCES = ["api.cu", "select_kernels.cu", "attn_simt.cu", "attn_sm100.cu", "attn_sm100_2cta.cu", "attn_sm100_pp.cu", "attn_sm100_pps.cu", "block_mass_sm100.cu"]
+SOURCES = ["api.cu", "select_kernels.cu", "attn_simt.cu", "attn_sm100.cu", "attn_sm100_pp.cu", "block_mass_sm100.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -32,8 +32,11 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, debug: bool = False, verbose: bool = True, extra_flags=None, out: str = None) -> str:
-    """extra_flags / out: A/B builds (e.g. -DBA_PP_PSPLIT=4 into another .so, loaded via BA_LIB_PATH)."""
+def build(force: bool = False, debug: bool = False, verbose: bool = True, extra_flags=None, out: str = None,
+          profiling: bool = False) -> str:
+    """extra_flags / out: A/B builds (e.g. -DBA_PP_PSPLIT=4 into another .so, loaded via BA_LIB_PATH).
+    profiling: also compile the profiling-only kernel variants (no-softmax skeleton, clock64 tile
+    traces with device printf; BA_ATTN_DEBUG=1|2) — never part of the product library."""
     lib = out or LIB
     if not force and not needs_build() and out is None:
         return LIB
@@ -42,6 +45,8 @@ def build(force: bool = False, debug: bool = False, verbose: bool = True, extra_
                     "-I", os.path.join(ROOT, "include"), "-Xptxas", "-v" if verbose and debug else "-O3"]
     if debug:
         flags += ["-DBA_DEBUG=1"]
+    if profiling:
+        flags += ["-DBA_PROFILING=1"]
     flags += list(extra_flags or [])
     t0 = time.time()
     procs = []
@@ -70,4 +75,5 @@ def build(force: bool = False, debug: bool = False, verbose: bool = True, extra_
 
 
 if __name__ == "__main__":
-    build(force=True, debug="--debug" in sys.argv)
+    build(force=True, debug="--debug" in sys.argv, profiling="--profiling" in sys.argv,
+          out=sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None)

@@ -201,6 +201,9 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   if (sel->q_sorted) BA_TRY(check_ptr("sel->q_sorted", sel->q_sorted));
   if (sel->k_sorted) BA_TRY(check_ptr("sel->k_sorted", sel->k_sorted));
   if (sel->v_sorted) BA_TRY(check_ptr("sel->v_sorted", sel->v_sorted));
+  if (D.nk > kSelectMaxNk)
+    return fail(BA_ERR_UNSUPPORTED, "ba_select supports N_k <= %lld key blocks (N_k = %lld): the top-kappa row "
+                "buffer is in shared memory", (long long)kSelectMaxNk, (long long)D.nk);
   const SelectPlan plan = plan_select(D, pa, sel);
   if (ws_bytes < plan.total)
     return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu < %zu", ws_bytes, plan.total);
@@ -306,10 +309,10 @@ AttnArgs make_attn_sorted(const Dims &D, const ba_params *pa, const ba_selection
 }
 
 // B = 128 kernel choice, BA_ATTN_K5 = "pp" (ping-pong pair, attn_sm100_pp.cu; the
-// default: +1.5-2% over 1cta on A and C), "2cta" (cluster pair,
-// attn_sm100_2cta.cu) or "1cta" (attn_sm100.cu).  The pair kernels walk the
-// union of two adjacent query blocks' lists.
-enum K5Kind { K5_1CTA = 0, K5_2CTA = 1, K5_PP = 2, K5_PPS = 3 };
+// default: +1.5-2% over 1cta on A and C) or "1cta" (attn_sm100.cu, also the
+// route for N_k > 8192, beyond the pair kernel's bitmask).  (Round 1's 2-CTA
+// cluster and smem-P variants measured slower and were removed.)
+enum K5Kind { K5_1CTA = 0, K5_PP = 2 };
 static const int kDefaultK5 = K5_PP;
 
 static int k5_kind() {
@@ -317,32 +320,78 @@ static int k5_kind() {
   if (kind < 0) {
     kind = kDefaultK5;
     const char *env = getenv("BA_ATTN_K5");
-    if (env && !strcmp(env, "pp")) kind = K5_PP;
-    else if (env && !strcmp(env, "pps")) kind = K5_PPS;
-    else if (env && !strcmp(env, "2cta")) kind = K5_2CTA;
-    else if (env && !strcmp(env, "1cta")) kind = K5_1CTA;
-    else if (getenv("BA_ATTN_2CTA") && atoi(getenv("BA_ATTN_2CTA"))) kind = K5_2CTA;
+    if (env && !strcmp(env, "1cta")) kind = K5_1CTA;
   }
   return kind;
 }
 
-bool use_pps(const AttnArgs &a) { return k5_kind() == K5_PPS && attn_pps_supported(a); }
-bool use_pp(const AttnArgs &a) { return (k5_kind() == K5_PP || (k5_kind() == K5_PPS && !attn_pps_supported(a))) && attn_pp_supported(a); }
-bool use_2cta(const AttnArgs &a) { return k5_kind() == K5_2CTA && attn_2cta_supported(a); }
+bool use_pp(const AttnArgs &a) { return k5_kind() == K5_PP && attn_pp_supported(a); }
+
+// bf16 with head_dim 128 must run on the tensor cores: the SIMT kernel serves
+// fp32 (config T) and bf16 head_dim 64 (no tcgen05 variant; documented in
+// ba_attn.h), never a bf16 d = 128 problem the tcgen05 kernels cannot take.
+const char *attn_unsupported(const AttnArgs &a) {
+  if (a.dtype == 0 && a.d == 128 && !attn_sm100_supported(a))
+    return "bf16 head_dim 128 attention supports N_k <= 32768 key blocks (the tcgen05 kernels' bitmask)";
+  return nullptr;
+}
 
 const char *attn_kernel_name(const AttnArgs &a) {
-  if (use_pps(a)) return "attn_sm100_tcgen05_pps";
+  if (attn_unsupported(a)) return "";
   if (use_pp(a)) return "attn_sm100_tcgen05_pp";
-  if (use_2cta(a)) return "attn_sm100_tcgen05_2cta";
   if (!attn_sm100_supported(a)) return "attn_simt";
   return (a.B == 64 && attn_sm100_dual64()) ? "attn_sm100_tcgen05_dual64" : "attn_sm100_tcgen05";
 }
 
-ba_status run_attn(const AttnArgs &a, cudaStream_t st) {
+// Device-detected errors (S:393 empty mask rows, out-of-range kv_index entries):
+// the attention kernels set bits of one process-wide word in mapped pinned
+// host memory (allocated once, like the copy streams below) and write a
+// deterministic result (an empty row gives O = 0, LSE = -inf; a bad index is
+// skipped); ba_check_errors, or the next attention call, reports them.
+std::mutex g_flag_mu;
+unsigned int *g_err_host = nullptr, *g_err_dev = nullptr;
+
+unsigned int *err_flag_dev() {
+  std::lock_guard<std::mutex> lock(g_flag_mu);
+  if (!g_err_host) {
+    void *p = nullptr;
+    if (cudaHostAlloc(&p, 2 * sizeof(unsigned int), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    g_err_host = static_cast<unsigned int *>(p);
+    reinterpret_cast<volatile unsigned int *>(g_err_host)[0] = 0u;
+    reinterpret_cast<volatile unsigned int *>(g_err_host)[1] = 0u;
+    void *d = nullptr;
+    if (cudaHostGetDevicePointer(&d, p, 0) != cudaSuccess) {
+      cudaGetLastError();
+      d = p;  // UVA: the host pointer is valid on the device
+    }
+    g_err_dev = static_cast<unsigned int *>(d);
+  }
+  return g_err_dev;
+}
+
+// Reads and clears the sticky bits (non-blocking: only work that has finished is seen).
+ba_status take_device_errors() {
+  if (!g_err_host) return BA_OK;
+  volatile unsigned int *f = g_err_host;
+  const unsigned int empty = f[kErrEmptyRow], bad = f[kErrBadIndex];
+  if (!empty && !bad) return BA_OK;
+  f[kErrEmptyRow] = 0u;
+  f[kErrBadIndex] = 0u;
+  if (empty)
+    return fail(BA_ERR_EMPTY_MASK_ROW, "an earlier attention launch met a query block with kv_count < 1 (S:393): "
+                                       "its rows were written as O = 0, LSE = -inf");
+  return fail(BA_ERR_INVALID_ARGUMENT, "an earlier attention launch met kv_index entries outside [0, N_k) "
+                                       "(skipped)");
+}
+
+ba_status run_attn(AttnArgs a, cudaStream_t st) {
+  if (const char *why = attn_unsupported(a)) return fail(BA_ERR_UNSUPPORTED, "%s", why);
+  a.err_flag = err_flag_dev();
   cudaError_t e;
-  if (use_pps(a)) e = launch_attn_pps(a, st);
-  else if (use_pp(a)) e = launch_attn_pp(a, st);
-  else if (use_2cta(a)) e = launch_attn_2cta(a, st);
+  if (use_pp(a)) e = launch_attn_pp(a, st);
   else if (attn_sm100_supported(a)) e = launch_attn_sm100(a, st);
   else e = launch_attn_simt(a, st);
   g_launches = 1;
@@ -379,7 +428,6 @@ bool dense_bh(const int64_t *s, int64_t H, int64_t L, int64_t d) {
 const char *gather_unsupported(const Dims &D, const ba_problem *prob, bool need_kv) {
   if (D.dtype != BA_DTYPE_BF16 || D.d != 128) return "zero-copy needs bf16 and head_dim 128 (tcgen05 path)";
   if (D.B == 64 && !attn_sm100_dual64()) return "zero-copy B = 64 needs the dual-tile kernel (BA_ATTN_B64 != pair)";
-  if (k5_kind() == K5_2CTA) return "the 2-CTA kernel (BA_ATTN_K5=2cta) reads permuted copies only";
   if (!dense_bh(prob->q_stride, D.hq, D.lq, D.d) ||
       (need_kv && (!dense_bh(prob->k_stride, D.hkv, D.lk, D.d) || !dense_bh(prob->v_stride, D.hkv, D.lk, D.d))))
     return "zero-copy needs q/k/v dense across (batch, head): stride[1] == L*stride[2], stride[0] == H*stride[1]";
@@ -431,6 +479,7 @@ ba_status run_sparse_gather(const Dims &D, const ba_problem *prob, const ba_para
   a.out = out;
   for (int i = 0; i < 3; ++i) a.os[i] = prob->o_stride[i];
   a.lse = lse;
+  a.err_flag = err_flag_dev();
   cudaError_t e = (D.B == 128 && use_pp(a)) ? launch_attn_pp(a, st) : launch_attn_sm100(a, st);
   g_launches = 1;
   return cuda_check(e, "attn_gather");
@@ -476,6 +525,7 @@ ba_status ba_select(const ba_problem *prob, const ba_params *params, const void 
 ba_status ba_sparse_attn(const ba_problem *prob, const ba_params *params, const ba_selection *sel, void *out,
                          float *lse, cudaStream_t stream) {
   g_err.clear();
+  BA_TRY(take_device_errors());
   Dims D;
   BA_TRY(check_problem(prob, params, &D));
   return run_sparse(D, prob, params, sel, out, lse, stream);
@@ -484,6 +534,7 @@ ba_status ba_sparse_attn(const ba_problem *prob, const ba_params *params, const 
 ba_status ba_sparse_attn_gather(const ba_problem *prob, const ba_params *params, const void *q, const void *k,
                                 const void *v, const ba_selection *sel, void *out, float *lse, cudaStream_t stream) {
   g_err.clear();
+  BA_TRY(take_device_errors());
   Dims D;
   BA_TRY(check_problem(prob, params, &D));
   return run_sparse_gather(D, prob, params, q, k, v, sel, out, lse, stream);
@@ -499,6 +550,7 @@ int ba_zero_copy_supported(const ba_problem *prob, const ba_params *params) {
 ba_status ba_sparse_attn_peers(const ba_problem *prob, const ba_params *params, const ba_selection *sel,
                                void *const *out_peers, int n_peers, float *lse, cudaStream_t stream) {
   g_err.clear();
+  BA_TRY(take_device_errors());
   Dims D;
   BA_TRY(check_problem(prob, params, &D));
   if (!out_peers || n_peers < 1 || n_peers > kMaxPeers)
@@ -512,7 +564,7 @@ ba_status ba_sparse_attn_peers(const ba_problem *prob, const ba_params *params, 
     return fail(BA_ERR_INVALID_ARGUMENT, "ba_sparse_attn_peers reads the permuted copies, kv_index, kv_count, perm_q");
   BA_TRY(check_strides("o", prob->o_stride, D.esz));
   AttnArgs a = make_attn_sorted(D, params, sel);
-  if (!attn_sm100_supported(a) || use_pps(a) || use_2cta(a))
+  if (!attn_sm100_supported(a))
     return fail(BA_ERR_UNSUPPORTED, "peer stores need the bf16 tcgen05 pair / single-CTA kernels (d = 128)");
   a.out = out_peers[0];
   a.n_peers = n_peers;
@@ -533,6 +585,7 @@ ba_status ba_sparse_attn_units(const ba_problem *prob, const ba_params *params, 
                                int64_t unit_begin, int64_t unit_end, void *const *out, int n_out, float *lse,
                                cudaStream_t stream) {
   g_err.clear();
+  BA_TRY(take_device_errors());
   Dims D;
   BA_TRY(check_problem(prob, params, &D));
   const int64_t n_units = D.b * D.hq * D.nq;
@@ -550,7 +603,7 @@ ba_status ba_sparse_attn_units(const ba_problem *prob, const ba_params *params, 
     return fail(BA_ERR_INVALID_ARGUMENT, "ba_sparse_attn_units reads the permuted copies, kv_index, kv_count, perm_q");
   BA_TRY(check_strides("o", prob->o_stride, D.esz));
   AttnArgs base = make_attn_sorted(D, params, sel);
-  if (n_out > 1 && (!attn_sm100_supported(base) || use_pps(base) || use_2cta(base)))
+  if (n_out > 1 && !attn_sm100_supported(base))
     return fail(BA_ERR_UNSUPPORTED, "peer stores need the bf16 tcgen05 pair / single-CTA kernels (d = 128)");
   for (int i = 0; i < 3; ++i) base.os[i] = prob->o_stride[i];
   const int64_t grp = D.hq / D.hkv;
@@ -595,6 +648,7 @@ ba_status ba_attention(const ba_problem *prob, const ba_params *params, const vo
                        const void *v, void *out, float *lse, void *workspace, size_t workspace_bytes,
                        cudaStream_t stream) {
   g_err.clear();
+  BA_TRY(take_device_errors());
   Dims D;
   BA_TRY(check_problem(prob, params, &D));
   // Permuted copies by default.  BA_ZERO_COPY=1: Q, K, V read through the permutations
@@ -648,6 +702,7 @@ ba_status ba_attention(const ba_problem *prob, const ba_params *params, const vo
 ba_status ba_dense_attn(const ba_problem *prob, const ba_params *params, const void *q, const void *k,
                         const void *v, void *out, float *lse, cudaStream_t stream) {
   g_err.clear();
+  BA_TRY(take_device_errors());
   Dims D;
   BA_TRY(check_problem(prob, params, &D));
   BA_TRY(check_ptr("q", q));
@@ -845,7 +900,84 @@ ba_status ba_block_mass(const ba_problem *prob, const ba_params *params, const b
   return BA_OK;
 }
 
+// NEXT-3: Eq. logits-bound U and the observed max logit deviation (Fig. 2)
+namespace {
+struct DevPlan {
+  size_t rq, mq, rk, mk, logit, smax, smin, total;
+};
+DevPlan plan_deviation(const Dims &D) {
+  DevPlan p{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
+  const size_t nqb = 8ull * D.b * D.hq * D.nq, nkb = 8ull * D.b * D.hkv * D.nk, pairs = (size_t)D.b * D.hq * D.nq * D.nk;
+  p.rq = take(nqb); p.mq = take(nqb); p.rk = take(nkb); p.mk = take(nkb);
+  p.logit = take(8 * pairs); p.smax = take(4 * pairs); p.smin = take(4 * pairs);
+  p.total = off;
+  return p;
+}
+}  // namespace
+
+size_t ba_deviation_workspace_size(const ba_problem *prob, const ba_params *params) {
+  Dims D;
+  if (check_problem(prob, params, &D) != BA_OK) return 0;
+  return plan_deviation(D).total;
+}
+
+ba_status ba_deviation(const ba_problem *prob, const ba_params *params, const ba_selection *sel, double *bound_u,
+                       double *max_dev, void *workspace, size_t workspace_bytes, cudaStream_t stream) {
+  g_err.clear();
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  if (D.dtype != BA_DTYPE_BF16 || D.d != 128 || D.B != 128)
+    return fail(BA_ERR_UNSUPPORTED, "ba_deviation: bf16, head_dim 128, block_size 128 (tcgen05 S pass)");
+  if (D.nk > 32 * 1024) return fail(BA_ERR_UNSUPPORTED, "ba_deviation: N_k > 32768");
+  if (!sel || !sel->q_sorted || !sel->k_sorted || !sel->q_mean || !sel->k_mean)
+    return fail(BA_ERR_INVALID_ARGUMENT, "ba_deviation reads sel->q_sorted/k_sorted/q_mean/k_mean (ba_select diagnostics)");
+  if (!bound_u && !max_dev) return fail(BA_ERR_INVALID_ARGUMENT, "bound_u and max_dev are both NULL");
+  const DevPlan pl = plan_deviation(D);
+  if (workspace_bytes < pl.total) return fail(BA_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes = %zu < %zu", workspace_bytes, pl.total);
+  if (!workspace) return fail(BA_ERR_INVALID_ARGUMENT, "workspace is NULL");
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return fail(BA_ERR_SHAPE_MISMATCH, "workspace is not 256-byte aligned");
+  double *rq = at<double>(workspace, pl.rq), *mq = at<double>(workspace, pl.mq);
+  double *rk = at<double>(workspace, pl.rk), *mk = at<double>(workspace, pl.mk);
+  double *logit = at<double>(workspace, pl.logit);
+  float *smax = at<float>(workspace, pl.smax), *smin = at<float>(workspace, pl.smin);
+  int launches = 0;
+  // R, M per block of the sorted copies, against the selection's fp64 block means
+  BA_TRY(cuda_check(launch_block_radius(D.dtype, (int)D.d, sel->q_sorted, D.b * D.hq, D.lq, (int)D.B, sel->q_mean, rq, mq,
+                                        stream), "block_radius(q)"));
+  BA_TRY(cuda_check(launch_block_radius(D.dtype, (int)D.d, sel->k_sorted, D.b * D.hkv, D.lk, (int)D.B, sel->k_mean, rk, mk,
+                                        stream), "block_radius(k)"));
+  launches += 2;
+  if (max_dev) {
+    // l = Qbar.Kbar / sqrt(d) (Eq. block-logit, no compensation), fp64 DMMA
+    BA_TRY(cuda_check(launch_scores((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, sel->q_mean, sel->q_mean, sel->k_mean,
+                                    sel->k_mean, 0, 0.0, logit, stream), "scores(l)"));
+    // the token-logit extremes per block pair: a dense S = Q'K'^T pass on the tensor cores
+    MassArgs m{};
+    m.d = (int)D.d; m.B = (int)D.B;
+    m.batch = D.b; m.hq = D.hq; m.hkv = D.hkv; m.lq = D.lq; m.lk = D.lk; m.nq = D.nq; m.nk = D.nk;
+    m.q = sel->q_sorted; m.k = sel->k_sorted;
+    m.qs[0] = D.hq * D.lq * D.d; m.qs[1] = D.lq * D.d; m.qs[2] = D.d;
+    m.ks[0] = D.hkv * D.lk * D.d; m.ks[1] = D.lk * D.d; m.ks[2] = D.d;
+    m.scale = 1.f;
+    m.s_max = smax; m.s_min = smin;
+    BA_TRY(cuda_check(launch_block_mass(m, stream), "logit_extremes"));
+    launches += 2;
+  }
+  BA_TRY(cuda_check(launch_deviation_finalize(D.b, D.hq, D.hkv, D.nq, D.nk, rq, mq, rk, mk, logit, smax, smin,
+                                              1.0 / sqrt((double)D.d), bound_u, max_dev, stream), "deviation"));
+  g_launches = launches + 1;
+  return BA_OK;
+}
+
 int ba_last_launch_count(void) { return g_launches; }
+
+ba_status ba_check_errors(cudaStream_t stream) {
+  g_err.clear();
+  BA_TRY(cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"));
+  return take_device_errors();
+}
 
 const char *ba_attention_kernel_name(const ba_problem *prob, const ba_params *params) {
   Dims D;

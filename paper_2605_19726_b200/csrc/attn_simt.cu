@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kSimtThreads) attn_simt_kernel(AttnArgs a) {
   }
   const int64_t row = (bh * a.nq + gq);
   const int cnt = a.kv_index ? (a.kv_count ? a.kv_count[row] : (int)a.kv_stride) : (int)a.nk;
+  if (cnt < 1 && threadIdx.x == 0) flag_error(a.err_flag, kErrEmptyRow);  // S:393; rows -> O = 0, LSE = -inf
   double m = -INFINITY;
   Acc l = 0;
   Acc acc[D];
@@ -52,6 +53,10 @@ __global__ void __launch_bounds__(kSimtThreads) attn_simt_kernel(AttnArgs a) {
   for (int c = 0; c < D; ++c) acc[c] = 0;
   for (int s = 0; s < cnt; ++s) {
     const int64_t gk = a.kv_index ? a.kv_index[row * a.kv_stride + s] : s;
+    if (gk < 0 || gk >= a.nk) {  // uniform across the CTA: every thread reads the same entry
+      if (threadIdx.x == 0) flag_error(a.err_flag, kErrBadIndex);
+      continue;
+    }
     const int64_t k0 = gk * a.B;
     const int nk = (int)imin64(a.B, a.lk - k0);
     for (int c0 = 0; c0 < nk; c0 += kSimtChunk) {
@@ -102,13 +107,13 @@ __global__ void __launch_bounds__(kSimtThreads) attn_simt_kernel(AttnArgs a) {
     const int64_t srow = row0 + i;
     const int64_t orow = a.perm_q ? a.perm_q[bh * a.lq + srow] : srow;
     T *o = static_cast<T *>(a.out) + b * a.os[0] + h * a.os[1] + orow * a.os[2];
-    const Acc inv = (Acc)1 / l;
+    const Acc inv = l > (Acc)0 ? (Acc)1 / l : (Acc)0;  // empty row: O = 0, LSE = -inf
 #pragma unroll
     for (int c = 0; c < D; ++c) {
       if constexpr (sizeof(T) == 4) o[c] = (float)(acc[c] * inv);
       else o[c] = __float2bfloat16_rn((float)(acc[c] * inv));
     }
-    if (a.lse) a.lse[bh * a.lq + orow] = (float)(m + log((double)l));
+    if (a.lse) a.lse[bh * a.lq + orow] = l > (Acc)0 ? (float)(m + log((double)l)) : -INFINITY;
   }
 }
 

@@ -167,9 +167,11 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
     uint32_t *m = q2 ? mask_b : mask_a;
     if (a.kv_index) {
       const int cnt = a.kv_count ? a.kv_count[row] : (int)a.kv_stride;
+      if (cnt < 1 && threadIdx.x == 0) flag_error(a.err_flag, kErrEmptyRow);  // S:393; rows -> O = 0, LSE = -inf
       const int32_t *idx = a.kv_index + row * a.kv_stride;
       for (int e = threadIdx.x; e < cnt; e += kThreads) {
         const int g = idx[e];
+        if ((unsigned)g >= (unsigned)a.nk) { flag_error(a.err_flag, kErrBadIndex); continue; }
         atomicOr(&m[g >> 5], 1u << (g & 31));
       }
     } else {  // dense: every key block
@@ -516,8 +518,8 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
       tmem_wait_ld();
       uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        pk[i] = pack_bf16(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
+      for (int i = 0; i < 16; ++i)  // lt == 0 (empty row): zeros, never unwritten TMEM x 0
+        pk[i] = lt > 0.f ? pack_bf16(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv) : 0u;
       if (r < nrows) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -642,6 +644,7 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
     const char *d = getenv("BA_ATTN_DEBUG");
     dbg = d ? atoi(d) : 0;
   }
+  (void)dbg;
   if (a.gather) {  // zero-copy: B = 128 single-block tiles, or B = 64 dual tiles
     if (a.B == 64 && !attn_sm100_dual64()) return cudaErrorNotSupported;
     // same exp2-offload variant as the copy path, so both paths are bit-identical
@@ -674,18 +677,22 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
     return cudaErrorInvalidValue;
   if (a.B == 64) {
     if (b64 == 0) return launch_variant<64, 0, false, false>(a, mk, mv, st);
+#ifdef BA_PROFILING
     if (dbg == 1) {
       AttnArgs b2 = a;
       const char *sk = getenv("BA_ATTN_SKIPLOAD");
       b2.dbg_flags = sk ? atoi(sk) : 0;
       return launch_variant<128, 0, true, false, true>(b2, mk, mv, st);
     }
+#endif
     switch (emu64) {  // exp2 offload for the dual-tile kernel (BA_EXP_EMU; default kDefaultEmu64)
       case 0: return launch_variant<128, 0, false, false, true>(a, mk, mv, st);
       case 2: return launch_variant<128, 2, false, false, true>(a, mk, mv, st);
       default: return launch_variant<128, 1, false, false, true>(a, mk, mv, st);
     }
   }
+#ifdef BA_PROFILING
+  // profiling-only variants (build with -DBA_PROFILING): no softmax (=1), tile trace (=2)
   if (dbg == 1) {
     AttnArgs b2 = a;
     const char *sk = getenv("BA_ATTN_SKIPLOAD");
@@ -693,6 +700,7 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
     return launch_variant<128, 0, true, false>(b2, mk, mv, st);
   }
   if (dbg == 2) return launch_variant<128, 0, false, true>(a, mk, mv, st);
+#endif
   switch (emu) {
     case 1: return launch_variant<128, 1, false, false>(a, mk, mv, st);
     case 2: return launch_variant<128, 2, false, false>(a, mk, mv, st);

@@ -84,7 +84,6 @@ struct __align__(8) Bars {
   uint64_t q_full;
   uint64_t full[NSLOT], empty[NSLOT];
   uint64_t s_full[2], p_part[2][kPSplit];    // per query block (A, B); p_part[q]: P of key part q in TMEM
-  uint64_t tok[2][4];             // MUFU token per SMSP: softmax A(u) -> B(u) -> A(u+1) ...
   uint64_t o_final;
   uint32_t tmem_base;
   uint32_t n_union;
@@ -114,13 +113,7 @@ struct UnionWalk {
 // fetched through pi_q / pi_k by the producer warp's 32 lanes (4 rows each of
 // every 128-row tile) with TMA tile::gather4 on 2-D maps over the (b*H*L, d)
 // row space; otherwise tile loads of the permuted copies.
-// kSeq: the "sequential" softmax organisation — all 8 softmax warps work on
-// block A's tile, then on block B's, each warp owning a 64-column half of its
-// lane quadrant's rows (two warps per SMSP in every exp phase, so each fills
-// the other's MUFU issue gaps); the row max is exchanged through shared memory
-// between the two warps of a quadrant.  The K/V ring shrinks to 4 slots to make
-// room for the exchange buffer.
-template <int kMode, int kEmu, bool kStagger = true, int kGather = 0, bool kSeq = false>
+template <int kMode, int kEmu, int kGather = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v) {
@@ -134,8 +127,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
   uint32_t *mask_b = mask_a + kMaskWords;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kSlots = kSeq ? NSLOT - 1 : NSLOT;  // kSeq: the last slot holds the max exchange
-  static_assert(!kSeq || kPSplit == 2, "kSeq publishes P by column half");
+  constexpr int kSlots = NSLOT;
   constexpr bool kTrace = kMode == 2;
   long long(*trace)[kTraceTiles] = reinterpret_cast<long long(*)[kTraceTiles]>(smem + SMEM_TRACE);
   const bool tr = kTrace && blockIdx.x == 0 && blockIdx.y == 0;
@@ -157,9 +149,11 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     uint32_t *m = q2 ? mask_b : mask_a;
     if (a.kv_index) {
       const int cnt = a.kv_count ? a.kv_count[row] : (int)a.kv_stride;
+      if (cnt < 1 && threadIdx.x == 0) flag_error(a.err_flag, kErrEmptyRow);  // S:393; rows -> O = 0, LSE = -inf
       const int32_t *idx = a.kv_index + row * a.kv_stride;
       for (int e = threadIdx.x; e < cnt; e += kThreads) {
         const int g = idx[e];
+        if ((unsigned)g >= (unsigned)a.nk) { flag_error(a.err_flag, kErrBadIndex); continue; }
         atomicOr(&m[g >> 5], 1u << (g & 31));
       }
     } else {
@@ -183,7 +177,6 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         mbar_init(&bars.s_full[s], 1);
         for (int q = 0; q < kPSplit; ++q) mbar_init(&bars.p_part[s][q], 4);
       }
-      for (int s = 0; s < 8; ++s) mbar_init(&bars.tok[s >> 2][s & 3], 1);
       mbar_init(&bars.o_final, 1);
       fence_barrier_init();
       tma_prefetch(&tm_q);
@@ -349,151 +342,6 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
   }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
-    if constexpr (kSeq) {
-    // ================================================================ softmax (sequential, column halves)
-    // warp w: TMEM lane quadrant qd = w % 4 (rows qd*32 + lane of BOTH blocks), key / column
-    // half ch = w / 4 of every tile; tiles A(u), B(u), A(u+1), ... in order
-    const int qd = warp & 3, ch = warp >> 2;
-    const int r = qd * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
-    float *xch = reinterpret_cast<float *>(smem + SMEM_SLOT + kSlots * TILE);  // [x][half][row]
-    const bool last_ragged = bars.last_ragged != 0u;
-    const int64_t ragged_valid = a.lk - (a.nk - 1) * (int64_t)BN;
-    const float c = a.scale * 1.4426950408889634f;
-    float mx[2] = {-INFINITY, -INFINITY}, lx[2] = {0.f, 0.f};
-    uint32_t sr[64];
-    UnionWalk walk;
-    walk.init(mask_a, mask_b);
-    for (int u = 0; u < cnt; ++u) {
-      const int gk = walk.next();
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        const uint32_t *my_mask = x ? mask_b : mask_a;
-        const bool mine = (my_mask[gk >> 5] >> (gk & 31)) & 1u;  // uniform over the 8 warps
-        const uint32_t scol = s_col(x), ocol = O_COL0 + 128 * x;
-        const bool trx = kTrace && warp == 0 && lane == 0;
-        mbar_wait(&bars.s_full[x], (uint32_t)u & 1u);
-        if (trx) TR(4 + 4 * x, u);
-        tc_fence_after();
-        if (kMode == 1) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) sr[i] = 0u;
-          if (mine) lx[x] = 1.f, mx[x] = 0.f;
-        } else if (mine) {
-          tmem_ld_x32(trow + scol + 64 * ch, sr);
-          tmem_ld_x32(trow + scol + 64 * ch + 32, sr + 32);
-          tmem_wait_ld();
-          if (trx) TR(5 + 4 * x, u);
-          if (last_ragged && u == cnt - 1) {
-#pragma unroll
-            for (int i = 0; i < 64; ++i)
-              if (64 * ch + i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
-          }
-          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-          for (int i = 0; i < 64; i += 8) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) m4[v] = fmax3(m4[v], __uint_as_float(sr[i + 2 * v]), __uint_as_float(sr[i + 2 * v + 1]));
-          }
-          const float hm = fmaxf(fmax3(m4[0], m4[1], m4[2]), m4[3]) * c;
-          xch[(x * 2 + ch) * 128 + r] = hm;
-          named_bar_sync(1 + qd, 64);  // the two column halves of these rows
-          const float mt = fmaxf(hm, xch[(x * 2 + (ch ^ 1)) * 128 + r]);
-          float m = mx[x];
-          if (m == -INFINITY) {
-            m = mt;  // first tile of these rows: O rows are still zero (earlier P rows were 0)
-          } else {
-            const bool need = mt > m + kRescaleThreshold;  // identical in both halves of a row
-            if (__any_sync(0xffffffffu, need)) {
-              // PV_x(u-1) is complete: the commit behind s_full[x](u) tracks every earlier MMA
-              float corr = 1.f;
-              if (need) { corr = ex2(m - mt); m = mt; }
-              uint32_t ov[16];
-#pragma unroll
-              for (int q8 = 0; q8 < 4; ++q8) {  // this half's 64 O columns
-                tmem_ld_x16(trow + ocol + 64 * ch + q8 * 16, ov);
-                tmem_wait_ld();
-#pragma unroll
-                for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
-                tmem_st_x16(trow + ocol + 64 * ch + q8 * 16, ov);
-              }
-              lx[x] *= corr;
-            }
-          }
-          mx[x] = m;
-          const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
-          uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
-            uint64_t p2;
-            if ((i & 7) < kEmu) {
-              p2 = exp2_poly2(x2);
-            } else {
-              float x0, x1;
-              unf2(x2, x0, x1);
-              p2 = f2(ex2(x0), ex2(x1));
-            }
-            acc2[i & 3] = fadd2(acc2[i & 3], p2);
-            float p0, p1;
-            unf2(p2, p0, p1);
-            sr[i] = pack_bf16(p0, p1);
-          }
-          const uint64_t t2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
-          float a0, a1;
-          unf2(t2, a0, a1);
-          lx[x] += a0 + a1;
-          if (trx) TR(6 + 4 * x, u);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) sr[i] = 0u;  // block not selected by these rows: P = 0
-        }
-        // P (bf16 pairs) of keys 64ch.. over S in TMEM (columns 32ch..), then p_part[x][ch]
-        tmem_st_x32(trow + scol + 32 * ch, sr);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars.p_part[x][ch]);
-        if (trx) TR(7 + 4 * x, u);
-      }
-    }
-    if (cnt > 0) {
-      mbar_wait(&bars.o_final, 0);
-      tc_fence_after();
-    }
-    // row sums: the two halves' partial l (same scale), exchanged once
-    xch[(0 * 2 + ch) * 128 + r] = lx[0];
-    xch[(1 * 2 + ch) * 128 + r] = lx[1];
-    named_bar_sync(1 + qd, 64);
-#pragma unroll
-    for (int x = 0; x < 2; ++x) {
-      const float l = lx[x] + xch[(x * 2 + (ch ^ 1)) * 128 + r];
-      const float m = mx[x];
-      const uint32_t ocol = O_COL0 + 128 * x;
-      const int64_t row0 = (ga + x) * (int64_t)BM;
-      const int nrows = (int)imin64(BM, a.lq - row0);
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      int64_t orow = row0 + r;
-      if (r < nrows && a.perm_q) orow = a.perm_q[bh * a.lq + row0 + r];
-      const int64_t o_off = b * a.os[0] + h * a.os[1] + orow * a.os[2];
-#pragma unroll
-      for (int q4 = 0; q4 < 2; ++q4) {
-        uint32_t ov[32];
-        tmem_ld_x32(trow + ocol + 64 * ch + q4 * 32, ov);
-        tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
-        if (r < nrows) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            store_out_row16<__nv_bfloat16>(a, o_off + 64 * ch + q4 * 32 + 8 * i,
-                                           make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
-        }
-      }
-      if (a.lse && ch == 0 && r < nrows) a.lse[bh * a.lq + orow] = l > 0.f ? (m + log2f(l)) * 0.69314718055994531f : -INFINITY;
-    }
-    } else {
     // ================================================================ softmax + epilogue
     const int x = warp >> 2;            // 0: block A, 1: block B
     const int qd = warp & 3;            // TMEM lane quadrant
@@ -510,18 +358,6 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     uint32_t sr[128];
     UnionWalk walk;
     walk.init(mask_a, mask_b);
-    // MUFU stagger: the A and B softmax warps sharing an SMSP (same qd) take turns
-    // on the exp section, A(u), B(u), A(u+1), ... so that one exponentiates while
-    // the tensor pipe runs the other's PV + next S (the tile trace showed both in
-    // phase, splitting MUFU, with the tensor pipe idle meanwhile).
-    auto take_token = [&](int u) {
-      if (x == 1) mbar_wait(&bars.tok[1][qd], (uint32_t)u & 1u);
-      else if (u > 0) mbar_wait(&bars.tok[0][qd], (uint32_t)(u - 1) & 1u);
-    };
-    auto give_token = [&]() {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars.tok[x ^ 1][qd]);
-    };
     // P (bf16 pairs) over S in TMEM: part q = keys 128q/kPSplit .. -> columns 64q/kPSplit ..
     // (S of those columns is already in registers), then p_part[q]
     auto publish_part = [&](int q) {
@@ -584,7 +420,6 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
             l *= corr;
           }
         }
-        if (kStagger) take_token(u);
         const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
@@ -612,10 +447,8 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         float a0, a1;
         unf2(t2, a0, a1);
         l += a0 + a1;
-        if (kStagger) give_token();
         if (trx) TR(6 + 4 * x, u);
       } else {
-        if (kStagger) { take_token(u); give_token(); }
 #pragma unroll
         for (int i = 0; i < 64; ++i) sr[i] = 0u;  // block not selected by these rows: P = 0
 #pragma unroll
@@ -643,7 +476,8 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       tmem_wait_ld();
       uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
+      for (int i = 0; i < 16; ++i)  // l == 0 (empty row): zeros, never unwritten TMEM x 0
+        pk[i] = l > 0.f ? pack_bf16(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv) : 0u;
       if (r < nrows) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -651,8 +485,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       }
     }
     if (a.lse && r < nrows) a.lse[bh * a.lq + orow] = l > 0.f ? (m + log2f(l)) * 0.69314718055994531f : -INFINITY;
-      }
-}
+  }
   tc_fence_before();
   __syncthreads();
   if (kTrace && tr && threadIdx.x == 0) {
@@ -676,29 +509,29 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
 
 namespace sm100 {
 namespace pp {
-template <int kMode, int kEmu, bool kStagger = true, int kGather = 0, bool kSeq = false>
+template <int kMode, int kEmu, int kGather = 0>
 cudaError_t launch_mode(const AttnArgs &a, const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, dim3 grid,
                         cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel<kMode, kEmu, kStagger, kGather, kSeq>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel<kMode, kEmu, kGather>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  attn_pp_kernel<kMode, kEmu, kStagger, kGather, kSeq><<<grid, kThreads, SMEM_BYTES, st>>>(a, mq, mk, mv);
+  attn_pp_kernel<kMode, kEmu, kGather><<<grid, kThreads, SMEM_BYTES, st>>>(a, mq, mk, mv);
   return cudaGetLastError();
 }
 }  // namespace pp
 }  // namespace sm100
 
-// BA_EXP_EMU (0..5; the gather paths support 0..2 and use 1 otherwise), read once
+// BA_EXP_EMU (0..3), read once
 static int emu_choice() {
   static int emu = -1;
   if (emu < 0) {
     const char *e = getenv("BA_EXP_EMU");
     emu = e ? atoi(e) : sm100::pp::kDefaultEmu;
-    if (emu < 0 || emu > 5) emu = sm100::pp::kDefaultEmu;
+    if (emu < 0 || emu > 3) emu = sm100::pp::kDefaultEmu;
   }
   return emu;
 }
@@ -712,72 +545,37 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
   using namespace sm100::pp;
   CUtensorMap mq, mk, mv;
   if (!get_encode()) return cudaErrorNotSupported;
+  const int emu = emu_choice();
+  dim3 grid((unsigned)((a.nq + 1) / 2), (unsigned)(a.batch * a.hq));
   if (a.gather) {  // bit 1: Q through pi_q (gather4); bit 2: K, V through pi_k (gather4)
     const bool gq = a.gather & 1, gkv = a.gather & 2;
     const bool ok = (gq ? make_gather_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs) : make_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs, 128)) &&
                     (gkv ? make_gather_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks) && make_gather_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs)
                          : make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) && make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128));
     if (!ok) return cudaErrorInvalidValue;
-    dim3 grid((unsigned)((a.nq + 1) / 2), (unsigned)(a.batch * a.hq));
-    // the copy path's exp2-offload variant (0..2), so both paths are bit-identical
-    const int e = emu_choice();
-    if (gq && gkv) {
-      if (e == 0) return launch_mode<0, 0, false, 3>(a, mq, mk, mv, grid, st);
-      if (e == 2) return launch_mode<0, 2, false, 3>(a, mq, mk, mv, grid, st);
-      return launch_mode<0, 1, false, 3>(a, mq, mk, mv, grid, st);
-    }
-    if (gkv) {
-      if (e == 0) return launch_mode<0, 0, false, 2>(a, mq, mk, mv, grid, st);
-      if (e == 2) return launch_mode<0, 2, false, 2>(a, mq, mk, mv, grid, st);
-      return launch_mode<0, 1, false, 2>(a, mq, mk, mv, grid, st);
-    }
-    if (e == 0) return launch_mode<0, 0, false, 1>(a, mq, mk, mv, grid, st);
-    if (e == 2) return launch_mode<0, 2, false, 1>(a, mq, mk, mv, grid, st);
-    return launch_mode<0, 1, false, 1>(a, mq, mk, mv, grid, st);
+    // the copy path's exp2-offload variant, so both paths are bit-identical
+    if (gq && gkv) return emu == 0 ? launch_mode<0, 0, 3>(a, mq, mk, mv, grid, st) : launch_mode<0, 1, 3>(a, mq, mk, mv, grid, st);
+    if (gkv) return emu == 0 ? launch_mode<0, 0, 2>(a, mq, mk, mv, grid, st) : launch_mode<0, 1, 2>(a, mq, mk, mv, grid, st);
+    return emu == 0 ? launch_mode<0, 0, 1>(a, mq, mk, mv, grid, st) : launch_mode<0, 1, 1>(a, mq, mk, mv, grid, st);
   }
   if (!make_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs, 128) || !make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) ||
       !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128))
     return cudaErrorInvalidValue;
-  static int dbg = -1, stagger = 0, seq = 0;
-  const int emu = emu_choice();
+#ifdef BA_PROFILING
+  // profiling-only variants (build with -DBA_PROFILING): BA_ATTN_DEBUG=1 no softmax, =2 tile trace
+  static int dbg = -1;
   if (dbg < 0) {
-    const char *sq = getenv("BA_PP_SEQ");
-    seq = sq ? atoi(sq) : 0;
-    const char *sg = getenv("BA_PP_STAGGER");
-    stagger = sg ? atoi(sg) : 0;  // measured slower (a lone warp cannot issue MUFU back to back): opt-in
     const char *d = getenv("BA_ATTN_DEBUG");
     dbg = d ? atoi(d) : 0;
-    if (dbg < 0 || dbg > 2) dbg = 0;
-  }
-  dim3 grid((unsigned)((a.nq + 1) / 2), (unsigned)(a.batch * a.hq));
-  if (seq) {
-    if (dbg == 1) return launch_mode<1, 0, false, 0, true>(a, mq, mk, mv, grid, st);
-    if (dbg == 2) return launch_mode<2, kDefaultEmu, false, 0, true>(a, mq, mk, mv, grid, st);
-    switch (emu) {
-      case 0: return launch_mode<0, 0, false, 0, true>(a, mq, mk, mv, grid, st);
-      case 1: return launch_mode<0, 1, false, 0, true>(a, mq, mk, mv, grid, st);
-      case 2: return launch_mode<0, 2, false, 0, true>(a, mq, mk, mv, grid, st);
-      default: return launch_mode<0, 3, false, 0, true>(a, mq, mk, mv, grid, st);
-    }
   }
   if (dbg == 1) return launch_mode<1, 0>(a, mq, mk, mv, grid, st);
-  if (dbg == 2) return stagger ? launch_mode<2, kDefaultEmu>(a, mq, mk, mv, grid, st)
-                               : launch_mode<2, kDefaultEmu, false>(a, mq, mk, mv, grid, st);
-  if (stagger) {
-    switch (emu) {
-      case 0: return launch_mode<0, 0, true>(a, mq, mk, mv, grid, st);
-      case 1: return launch_mode<0, 1, true>(a, mq, mk, mv, grid, st);
-      case 2: return launch_mode<0, 2, true>(a, mq, mk, mv, grid, st);
-      default: return launch_mode<0, 3, true>(a, mq, mk, mv, grid, st);
-    }
-  }
+  if (dbg == 2) return launch_mode<2, kDefaultEmu>(a, mq, mk, mv, grid, st);
+#endif
   switch (emu) {  // of every 8 exp2 pairs, emu go to the FMA-pipe polynomial
-    case 0: return launch_mode<0, 0, false>(a, mq, mk, mv, grid, st);
-    case 1: return launch_mode<0, 1, false>(a, mq, mk, mv, grid, st);
-    case 2: return launch_mode<0, 2, false>(a, mq, mk, mv, grid, st);
-    case 3: return launch_mode<0, 3, false>(a, mq, mk, mv, grid, st);
-    case 4: return launch_mode<0, 4, false>(a, mq, mk, mv, grid, st);
-    default: return launch_mode<0, 5, false>(a, mq, mk, mv, grid, st);
+    case 0: return launch_mode<0, 0>(a, mq, mk, mv, grid, st);
+    case 1: return launch_mode<0, 1>(a, mq, mk, mv, grid, st);
+    case 2: return launch_mode<0, 2>(a, mq, mk, mv, grid, st);
+    default: return launch_mode<0, 3>(a, mq, mk, mv, grid, st);
   }
 }
 

@@ -3,6 +3,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifdef __CUDACC__
+#define BA_HOST_DEVICE_INLINE __host__ __device__ __forceinline__
+#else
+#define BA_HOST_DEVICE_INLINE inline
+#endif
+
 namespace baatt {
 
 // ---------------------------------------------------------------- sort geometry
@@ -70,6 +76,9 @@ cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t
                           const double *q_mean, const double *q_var, const double *k_mean,
                           const double *k_var, int comp, double beta, double *logits,
                           cudaStream_t st);
+// largest N_k the top-kappa kernel takes: one warp holds a row of N_k fp64 logits (+1 KB of
+// histograms) in shared memory (227 KB per CTA)
+constexpr int64_t kSelectMaxNk = 28672;
 // top_p > 0: cumulative-mass budget (reading A23), kappa = the cap and the kv_index row stride
 cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *logits,
                         int32_t *kv_index, int32_t *kv_count, uint8_t *mask, double *prob,
@@ -103,17 +112,23 @@ struct AttnArgs {
   // as out) instead of out — the peers' symmetric buffers, pre-offset to this rank's heads
   int n_peers;
   void *out_peers[kMaxPeers];
+  // device-detected errors (two mapped host words, or nullptr): word kErrEmptyRow is
+  // set when a query block's kv_count < 1 (its rows get O = 0, LSE = -inf), word
+  // kErrBadIndex when a kv_index entry is outside [0, N_k) (the entry is skipped).
+  // One word per error with plain idempotent stores: no read-modify-write, so no
+  // system-scope atomics over PCIe are needed.
+  unsigned int *err_flag;
 };
+constexpr int kErrEmptyRow = 0, kErrBadIndex = 1;
+BA_HOST_DEVICE_INLINE void flag_error(unsigned int *f, int which) {
+  if (f) reinterpret_cast<volatile unsigned int *>(f)[which] = 1u;
+}
 cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t st);
 cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st);
 bool attn_sm100_supported(const AttnArgs &a);
 bool attn_sm100_dual64();
-cudaError_t launch_attn_2cta(const AttnArgs &a, cudaStream_t st);
-bool attn_2cta_supported(const AttnArgs &a);
 cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st);
 bool attn_pp_supported(const AttnArgs &a);
-cudaError_t launch_attn_pps(const AttnArgs &a, cudaStream_t st);
-bool attn_pps_supported(const AttnArgs &a);
 
 // ---------------------------------------------------------------- NEXT-3: oracle block mass
 struct MassArgs {
@@ -126,11 +141,19 @@ struct MassArgs {
   const int32_t *kv_index;      // selection for the captured mass (or nullptr)
   const int32_t *kv_count;
   int64_t kv_stride;
-  float *m_hat;                 // [b, hq, nq, nk]
+  float *m_hat;                 // [b, hq, nq, nk] or nullptr (no mass pass)
   float *captured;              // [b, hq, nq] or nullptr
+  float *s_max, *s_min;         // [b, hq, nq, nk] token-logit extremes S = Q'.K' (unscaled), or nullptr
 };
 bool block_mass_supported(const MassArgs &a);
 cudaError_t launch_block_mass(const MassArgs &a, cudaStream_t st);
+// Eq. logits-bound: per-block radius R and max norm M (fp64) of a sorted copy
+cudaError_t launch_block_radius(int dtype, int d, const void *x, int64_t batch_heads, int64_t L, int B,
+                                const double *mean, double *R, double *M, cudaStream_t st);
+cudaError_t launch_deviation_finalize(int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk, const double *rq,
+                                      const double *mq, const double *rk, const double *mk, const double *logit,
+                                      const float *smax, const float *smin, double inv_sqrt_d, double *U, double *dev,
+                                      cudaStream_t st);
 
 }  // namespace baatt
 

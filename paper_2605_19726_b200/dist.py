@@ -64,11 +64,25 @@ def unit_heads(u0: int, u1: int, n_q: int, heads_q: int, heads_kv: int) -> Tuple
     return kv0 * grp, kv1 * grp, kv0, kv1
 
 
-def gather_units(out_full: torch.Tensor, group=None) -> torch.Tensor:
-    """Reassemble O after a unit split: every rank stored its units' rows into a
-    zero-filled full-size O and every row has exactly one writer, so a SUM
-    all-reduce reproduces the 1-GPU output bit for bit (x + 0 is exact)."""
-    dist.all_reduce(out_full, op=dist.ReduceOp.SUM, group=group)
+def gather_units(out_local: torch.Tensor, out_full: torch.Tensor = None, group=None) -> torch.Tensor:
+    """Reassemble O after a unit split.  out_local: this rank's zero-filled full-size
+    O into which only its own units' rows were ever stored; it is NOT modified, so
+    it can be reused step after step (its other rows stay zero).  Every row has
+    exactly one writer across the ranks, so a SUM reduction reproduces the 1-GPU
+    output bit for bit (x + 0 is exact).  out_full: the reassembled O (allocated
+    if None).  NCCL: an out-of-place all-reduce as reduce-scatter + all-gather of
+    the flat buffer; gloo: copy + in-place all-reduce."""
+    if out_full is None:
+        out_full = torch.empty_like(out_local)
+    world = dist.get_world_size(group)
+    flat, full = out_local.reshape(-1), out_full.view(-1)
+    if dist.get_backend(group) == "nccl" and flat.numel() % world == 0:
+        chunk = torch.empty(flat.numel() // world, dtype=flat.dtype, device=flat.device)
+        dist.reduce_scatter_tensor(chunk, flat, op=dist.ReduceOp.SUM, group=group)
+        dist.all_gather_into_tensor(full, chunk, group=group)
+    else:
+        out_full.copy_(out_local)
+        dist.all_reduce(out_full, op=dist.ReduceOp.SUM, group=group)
     return out_full
 
 

@@ -191,3 +191,32 @@ def test_units_validation_before_launch(ba):
     assert b"n_out" in lib.ba_last_error()
     st = lib.ba_sparse_attn_units(ctypes.byref(p), ctypes.byref(pa), ctypes.byref(sel), 0, n_units, outs, 1, None, None)
     assert lib.ba_status_string(st).decode() == "BA_ERR_INVALID_ARGUMENT"  # empty selection struct
+
+
+def test_no_silent_simt_for_bf16_d128(ba):
+    """bf16 with head_dim 128 always runs a tcgen05 kernel; beyond their N_k <= 32768
+    bitmask the attention calls return BA_ERR_UNSUPPORTED before any launch (no
+    silent SIMT fallback), and ba_select refuses N_k above its shared-memory
+    top-kappa capacity (28672) the same way.  Fake (never dereferenced) device
+    pointers: validation happens before any CUDA call."""
+    lib = ba.load()
+    q, k, v = _meta(1, 1, 1, 32769 * 128, 128)
+    assert ba.attention_kernel_name(q, k, v, 128) == ""
+    p, pa = ba.make_problem(q, k, v), ba.make_params()
+    fake = ctypes.c_void_p(1 << 20)
+    st = lib.ba_dense_attn(ctypes.byref(p), ctypes.byref(pa), fake, fake, fake, fake, None, None)
+    assert lib.ba_status_string(st).decode() == "BA_ERR_UNSUPPORTED"
+    assert b"32768" in lib.ba_last_error()
+    sel = ba.SelectionC()
+    for f in ("perm_q", "perm_k", "q_sorted", "k_sorted", "v_sorted", "kv_index", "kv_count"):
+        setattr(sel, f, 1 << 20)
+    st = lib.ba_sparse_attn(ctypes.byref(p), ctypes.byref(pa), ctypes.byref(sel), fake, None, None)
+    assert lib.ba_status_string(st).decode() == "BA_ERR_UNSUPPORTED"
+    q, k, v = _meta(1, 1, 1, 28673 * 128, 128)
+    p = ba.make_problem(q, k, v)
+    st = lib.ba_select(ctypes.byref(p), ctypes.byref(pa), fake, fake, fake, ctypes.byref(sel), fake, 1 << 40, None)
+    assert lib.ba_status_string(st).decode() == "BA_ERR_UNSUPPORTED"
+    assert b"28672" in lib.ba_last_error()
+    # bf16 head_dim 64 has no tcgen05 variant: the documented SIMT route, named as such
+    q, k, v = _meta(1, 2, 2, 4096, 64)
+    assert ba.attention_kernel_name(q, k, v, 128) == "attn_simt"

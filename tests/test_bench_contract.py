@@ -67,3 +67,22 @@ def test_bench_unit_split_single_rank():
                 "--no-dense"])
     assert d["scaling"] == "strong" and d["config"]["parallelism"].startswith("unit-parallel x1")
     assert d["flops_per_step_per_rank"] == base["flops_per_step_per_rank"]
+
+
+@pytest.mark.parametrize("args,par", [
+    (["--config", "C", "--seq-len", "2048", "--gpus", "2"], "head-parallel x2"),
+    (["--config", "C", "--seq-len", "1500", "--gpus", "4"], "head-parallel x4"),
+    (["--config", "M", "--seq-len", "1024", "--gpus", "3"], "unit-parallel x3"),
+])
+def test_bench_gpus_n_self_launches_ranks(args, par):
+    """`bench.py --gpus N` outside torchrun re-launches itself as N ranks
+    (torch.distributed.run) and defaults to the head-parallel strong-scaling split
+    with the output collective in the step; --dry-run runs the same launcher,
+    partition and reassembly on CPU (gloo) ranks with a stand-in kernel and
+    checks that every rank ends up with the whole layer's O."""
+    d = _bench(args + ["--dry-run", "--steps", "2", "--warmup", "1"], timeout=300)
+    n = int(args[args.index("--gpus") + 1])
+    assert d["n_gpus"] == n and d["scaling"] == "strong"
+    assert d["config"]["parallelism"].startswith(par)
+    assert d["dry_run"] == "reassembled O equals the 1-rank layout on every rank"
+    assert d["value"] is None  # a dry run is never a measurement

@@ -129,8 +129,12 @@ def _unit_worker(rank, world, port, q):
             h, gq = divmod(u, nq)
             rows = perm[h, gq * B:min(L, (gq + 1) * B)]
             mine[0, h, rows] = full[0, h, rows]
+        keep = mine.clone()
         got = gather_units(mine)
-        q.put((rank, torch.equal(got, full)))
+        ok = torch.equal(got, full) and torch.equal(mine, keep)  # out-of-place: the local rows stay as stored
+        # a second step on the same (unchanged) local buffer reassembles the same O (no stale rows summed in)
+        got2 = gather_units(mine, torch.empty_like(full))
+        q.put((rank, ok and torch.equal(got2, full)))
     finally:
         dist.destroy_process_group()
 
