@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbaatt.so")
-SOURCES = ["api.cu", "select_kernels.cu", "attn_simt.cu", "attn_sm100.cu", "attn_sm100_pp.cu", "block_mass_sm100.cu"]
+SOURCES = ["api.cu", "select_kernels.cu", "attn_simt.cu", "attn_sm100.cu", "attn_sm100_pp.cu", "attn_sm100_pp2.cu", "block_mass_sm100.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

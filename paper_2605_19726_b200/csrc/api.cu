@@ -312,7 +312,7 @@ AttnArgs make_attn_sorted(const Dims &D, const ba_params *pa, const ba_selection
 // default: +1.5-2% over 1cta on A and C) or "1cta" (attn_sm100.cu, also the
 // route for N_k > 8192, beyond the pair kernel's bitmask).  (Round 1's 2-CTA
 // cluster and smem-P variants measured slower and were removed.)
-enum K5Kind { K5_1CTA = 0, K5_PP = 2 };
+enum K5Kind { K5_1CTA = 0, K5_PP = 2, K5_PP2 = 3 };
 static const int kDefaultK5 = K5_PP;
 
 static int k5_kind() {
@@ -321,11 +321,15 @@ static int k5_kind() {
     kind = kDefaultK5;
     const char *env = getenv("BA_ATTN_K5");
     if (env && !strcmp(env, "1cta")) kind = K5_1CTA;
+    else if (env && !strcmp(env, "pp")) kind = K5_PP;
+    else if (env && !strcmp(env, "pp2")) kind = K5_PP2;
   }
   return kind;
 }
 
-bool use_pp(const AttnArgs &a) { return k5_kind() == K5_PP && attn_pp_supported(a); }
+// pp2: the pair kernel on a 2-CTA cluster (cta_group::2 MMAs, K/V halves per SM)
+bool use_pp2(const AttnArgs &a) { return k5_kind() == K5_PP2 && attn_pp2_supported(a); }
+bool use_pp(const AttnArgs &a) { return (k5_kind() == K5_PP || (k5_kind() == K5_PP2 && !use_pp2(a))) && attn_pp_supported(a); }
 
 // bf16 with head_dim 128 must run on the tensor cores: the SIMT kernel serves
 // fp32 (config T) and bf16 head_dim 64 (no tcgen05 variant; documented in
@@ -338,6 +342,7 @@ const char *attn_unsupported(const AttnArgs &a) {
 
 const char *attn_kernel_name(const AttnArgs &a) {
   if (attn_unsupported(a)) return "";
+  if (use_pp2(a)) return "attn_sm100_tcgen05_pp2";
   if (use_pp(a)) return "attn_sm100_tcgen05_pp";
   if (!attn_sm100_supported(a)) return "attn_simt";
   return (a.B == 64 && attn_sm100_dual64()) ? "attn_sm100_tcgen05_dual64" : "attn_sm100_tcgen05";
@@ -391,7 +396,8 @@ ba_status run_attn(AttnArgs a, cudaStream_t st) {
   if (const char *why = attn_unsupported(a)) return fail(BA_ERR_UNSUPPORTED, "%s", why);
   a.err_flag = err_flag_dev();
   cudaError_t e;
-  if (use_pp(a)) e = launch_attn_pp(a, st);
+  if (use_pp2(a)) e = launch_attn_pp2(a, st);
+  else if (use_pp(a)) e = launch_attn_pp(a, st);
   else if (attn_sm100_supported(a)) e = launch_attn_sm100(a, st);
   else e = launch_attn_simt(a, st);
   g_launches = 1;

@@ -48,6 +48,20 @@ cudaError_t launch_norm_keys(int dtype, int d, const void *x, const int64_t *str
                              cudaStream_t st);
 cudaError_t launch_radix_sort(const SortGeom &g, uint32_t *keys_a, uint32_t *vals_a, uint32_t *keys_b,
                               uint32_t *vals_b, uint32_t *hist, cudaStream_t st, int *launches);
+// K1 + K2 fused into 1 + 4 launches (+ 1 memset of the control block): the norm keys of the
+// sorted sides with their per-segment digit histograms, then four onesweep passes.
+// Side s of the SortGeom reads ka.x[s] with strides ka.st[s]; ka.user[s] (or NULL) gets a
+// copy of the keys in original order.
+struct KeysArgs {
+  const void *x[2];
+  int64_t st[2][3];
+  float *user[2];
+  int64_t batch;
+};
+size_t sort_ctrl_bytes(const SortGeom &g);
+cudaError_t launch_keys_sort(const SortGeom &g, int dtype, int d, const KeysArgs &ka, uint32_t *keys_a,
+                             uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, void *ctrl, cudaStream_t st,
+                             int *launches);
 cudaError_t launch_gather_stats(int dtype, int d, const void *x, const int64_t *stride, int64_t batch,
                                 int64_t heads, int64_t L, int B, const int32_t *perm,
                                 int32_t *perm_identity_out, void *xs, double *mean, double *var,
@@ -129,6 +143,8 @@ bool attn_sm100_supported(const AttnArgs &a);
 bool attn_sm100_dual64();
 cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st);
 bool attn_pp_supported(const AttnArgs &a);
+cudaError_t launch_attn_pp2(const AttnArgs &a, cudaStream_t st);
+bool attn_pp2_supported(const AttnArgs &a);
 
 // ---------------------------------------------------------------- NEXT-3: oracle block mass
 struct MassArgs {

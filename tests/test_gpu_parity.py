@@ -218,7 +218,7 @@ def test_injected_oracle_mask(ba):
     assert ref_sel  # oracle selection computed on the same inputs
 
 
-@pytest.mark.parametrize("B,k5", [(128, "1cta"), (128, "pp"), (64, "dual"), (64, "pair")])
+@pytest.mark.parametrize("B,k5", [(128, "1cta"), (128, "pp"), (128, "pp2"), (64, "dual"), (64, "pair")])
 def test_injected_dissimilar_lists(ba, B, k5):
     """Random (dissimilar) index lists for every query block: exercises the
     pair kernels' union walk where a block skips tiles (P = 0 rows), including
@@ -276,7 +276,8 @@ def test_errors_are_loud(ba):
         ba.ba_attention(q, k, v)
 
 
-@pytest.mark.parametrize("k5,name", [("pp", "attn_sm100_tcgen05_pp"), ("1cta", "attn_sm100_tcgen05")])
+@pytest.mark.parametrize("k5,name", [("pp", "attn_sm100_tcgen05_pp"), ("pp2", "attn_sm100_tcgen05_pp2"),
+                                     ("1cta", "attn_sm100_tcgen05")])
 def test_b128_kernel_parity(ba, k5, name):
     """Each B = 128 kernel (BA_ATTN_K5 = pp | 1cta) on real selections,
     ragged lengths, GQA and an odd number of query blocks."""
@@ -628,7 +629,8 @@ print("RESULT", ok1, ok2)
 
 
 # ---------------------------------------------------------------- boundary: S:393 empty rows, bad indices
-@pytest.mark.parametrize("cfg,B,k5", [("A", 128, "pp"), ("A", 128, "1cta"), ("M", 64, "dual"), ("T", 64, "simt")])
+@pytest.mark.parametrize("cfg,B,k5", [("A", 128, "pp"), ("A", 128, "pp2"), ("A", 128, "1cta"), ("M", 64, "dual"),
+                                      ("T", 64, "simt")])
 def test_empty_mask_row_is_reported(ba, cfg, B, k5):
     """An injected kv_count = 0 violates the non-empty-row precondition:
     the kernels write those rows as O = 0, LSE = -inf (never unwritten TMEM),
