@@ -433,7 +433,10 @@ def run_ours(args):
         if units is not None:
             ctx.sparse_attn_units(units[0], units[1], fused.peer_ptrs if fused is not None else [out])
         elif fused is not None:
-            ctx.sparse_attn_peers(fused.peer_ptrs)
+            if fused.mc_ptr:
+                ctx.sparse_attn_multicast(fused.mc_ptr)  # NVLS: one multimem.st per row reaches every rank
+            else:
+                ctx.sparse_attn_peers(fused.peer_ptrs)
         else:
             ctx.sparse_attn(out, sel=run_sel)
         return ba.last_launch_count()
@@ -654,7 +657,8 @@ def run_ours(args):
                       else "NCCL out-of-place SUM reduction of the zero-filled O)"))
         elif heads:
             par = (f"head-parallel x{world} (whole GQA groups per rank, "
-                   + ("O gathered by peer stores in the attention epilogue)" if fused is not None
+                   + (("O gathered by NVLS multimem.st in the attention epilogue)" if fused.mc_ptr else
+                       "O gathered by peer stores in the attention epilogue)") if fused is not None
                       else "NCCL all-gather of O)" if world > 1 else "one rank holds every head)"))
         else:
             par = f"batch-parallel x{world} (weak scaling, no data-path collective)"

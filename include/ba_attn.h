@@ -240,6 +240,18 @@ ba_status ba_sparse_attn_peers(const ba_problem *prob, const ba_params *params,
                                const ba_selection *sel, void *const *out_peers, int n_peers,
                                float *lse, cudaStream_t stream);
 
+/* As ba_sparse_attn_peers, but every output row is stored ONCE, with multimem.st
+ * (NVLS, NVLink SHARP), to out_multicast: a multicast device address (e.g. torch
+ * symmetric memory's multicast_ptr) pre-offset to this rank's head slice, so the
+ * NVSwitch replicates each store into every rank's copy — one store instruction
+ * and one NVLink egress per row instead of n_peers unicast stores.  Same layout
+ * rules as ba_sparse_attn_peers; bf16, head_dim 128 (tcgen05 kernels), else
+ * BA_ERR_UNSUPPORTED.  The caller orders the peers' reads after every rank's
+ * kernel (a symmetric-memory barrier). */
+ba_status ba_sparse_attn_multicast(const ba_problem *prob, const ba_params *params,
+                                   const ba_selection *sel, void *out_multicast, float *lse,
+                                   cudaStream_t stream);
+
 /* Alg. 1 steps 11-12 for a contiguous range of WORK UNITS only —
  * the uneven multi-GPU split of SURVEY §8(e) (e.g. 28 heads over 8 GPUs):
  * unit u = (b*H_q + h)*N_q + g_q is query block g_q of head h of batch b, and

@@ -92,6 +92,8 @@ def load() -> ctypes.CDLL:
     lib.ba_deviation.restype = ctypes.c_int
     lib.ba_sparse_attn_peers.argtypes = [P, PA, S, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, vp, st]
     lib.ba_sparse_attn_peers.restype = ctypes.c_int
+    lib.ba_sparse_attn_multicast.argtypes = [P, PA, S, vp, vp, st]
+    lib.ba_sparse_attn_multicast.restype = ctypes.c_int
     lib.ba_sparse_attn_units.argtypes = [P, PA, S, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p),
                                          ctypes.c_int, vp, st]
     lib.ba_sparse_attn_units.restype = ctypes.c_int
@@ -117,6 +119,7 @@ def load() -> ctypes.CDLL:
 
 EXPORTED = ["ba_abi_version", "ba_selection_sizes", "ba_select_workspace_size", "ba_attention_workspace_size",
             "ba_select", "ba_sparse_attn", "ba_sparse_attn_gather", "ba_sparse_attn_peers", "ba_sparse_attn_units",
+            "ba_sparse_attn_multicast",
             "ba_zero_copy_supported",
             "ba_attention", "ba_dense_attn", "ba_block_mass_workspace_size", "ba_block_mass",
             "ba_deviation_workspace_size", "ba_deviation",
@@ -381,6 +384,14 @@ class Context:
         arr = (ctypes.c_void_p * len(peer_ptrs))(*[ctypes.c_void_p(int(p)) for p in peer_ptrs])
         _check(load().ba_sparse_attn_peers(ctypes.byref(self.prob), ctypes.byref(self.params), ctypes.byref(self.sel_c),
                                            arr, len(peer_ptrs), _ptr(lse), _stream(stream)))
+
+    def sparse_attn_multicast(self, mc_ptr, lse=None, stream=None):
+        """Fused output collective over NVLS: every output row stored once with multimem.st
+        to the multicast address mc_ptr (ba_sparse_attn_multicast); strides those of `out`
+        given at construction."""
+        _check(load().ba_sparse_attn_multicast(ctypes.byref(self.prob), ctypes.byref(self.params),
+                                               ctypes.byref(self.sel_c), ctypes.c_void_p(int(mc_ptr)), _ptr(lse),
+                                               _stream(stream)))
 
     def sparse_attn_units(self, unit_begin: int, unit_end: int, outs, lse=None, stream=None):
         """Attention for work units [unit_begin, unit_end) only, u = (b*Hq + h)*Nq + g_q

@@ -145,7 +145,7 @@ SelectPlan plan_select(const Dims &D, const ba_params *pa, const ba_selection *s
   p.vals_a = take(4 * g.keys_total);
   p.keys_b = take(4 * g.keys_total);
   p.vals_b = take(4 * g.keys_total);
-  p.hist = take(4 * 256 * g.tiles_total);
+  p.hist = take(sort_ctrl_bytes(g));  // onesweep control block: segment histograms, look-back status, tickets
   const size_t qs = 8ull * D.b * D.hq * D.nq * D.d, ks = 8ull * D.b * D.hkv * D.nk * D.d;
   p.q_mean = (sel && sel->q_mean) ? SIZE_MAX : take(qs);
   p.q_var = (sel && sel->q_var) ? SIZE_MAX : take(qs);
@@ -215,30 +215,32 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   g.side[0].perm_out = nullptr;
   uint32_t *keys_a = at<uint32_t>(ws, plan.keys_a), *vals_a = at<uint32_t>(ws, plan.vals_a);
   uint32_t *keys_b = at<uint32_t>(ws, plan.keys_b), *vals_b = at<uint32_t>(ws, plan.vals_b);
-  // K1: norm keys (for every sorted side; also when the caller asked for them)
+  // K1 + K2: norm keys of the sorted sides with their digit histograms, then the four onesweep
+  // passes -> perm_q / perm_k (1 memset + 5 launches); keys of an unsorted side only when asked for
   {
+    KeysArgs ka{};
+    ka.batch = D.b;
     int si = 0;
     if (sort_q(pa)) {
       g.side[si].perm_out = sel->perm_q;
-      BA_TRY(cuda_check(launch_norm_keys(D.dtype, (int)D.d, q, prob->q_stride, D.b, D.hq, D.lq,
-                                         reinterpret_cast<float *>(keys_a) + g.side[si].base, sel->q_key, st), "norm_keys(q)"));
-      ++launches; ++si;
+      ka.x[si] = q; ka.user[si] = sel->q_key;
+      for (int i = 0; i < 3; ++i) ka.st[si][i] = prob->q_stride[i];
+      ++si;
     } else if (sel->q_key) {
       BA_TRY(cuda_check(launch_norm_keys(D.dtype, (int)D.d, q, prob->q_stride, D.b, D.hq, D.lq, sel->q_key, nullptr, st), "norm_keys(q)"));
       ++launches;
     }
     if (sort_k(pa)) {
       g.side[si].perm_out = sel->perm_k;
-      BA_TRY(cuda_check(launch_norm_keys(D.dtype, (int)D.d, k, prob->k_stride, D.b, D.hkv, D.lk,
-                                         reinterpret_cast<float *>(keys_a) + g.side[si].base, sel->k_key, st), "norm_keys(k)"));
-      ++launches;
+      ka.x[si] = k; ka.user[si] = sel->k_key;
+      for (int i = 0; i < 3; ++i) ka.st[si][i] = prob->k_stride[i];
     } else if (sel->k_key) {
       BA_TRY(cuda_check(launch_norm_keys(D.dtype, (int)D.d, k, prob->k_stride, D.b, D.hkv, D.lk, sel->k_key, nullptr, st), "norm_keys(k)"));
       ++launches;
     }
+    BA_TRY(cuda_check(launch_keys_sort(g, D.dtype, (int)D.d, ka, keys_a, vals_a, keys_b, vals_b, at<void>(ws, plan.hist), st,
+                                       &launches), "keys_sort"));
   }
-  // K2: stable segmented sort -> perm_q / perm_k
-  BA_TRY(cuda_check(launch_radix_sort(g, keys_a, vals_a, keys_b, vals_b, at<uint32_t>(ws, plan.hist), st, &launches), "radix_sort"));
   // K3: permuted copies + block statistics
   double *q_mean = sel->q_mean ? sel->q_mean : at<double>(ws, plan.q_mean);
   double *q_var = sel->q_var ? sel->q_var : at<double>(ws, plan.q_var);
@@ -263,8 +265,11 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
     BA_TRY(cuda_check(launch_gather_stats_multi(D.dtype, (int)D.d, gs, (int)D.B, st), "gather_stats"));
     ++launches;
   }
-  // K4: scores, then per-row top-kappa
+  // K4: scores, then per-row top-kappa — one cooperative launch (grid-wide barrier between them)
   double *logits = sel->logits ? sel->logits : at<double>(ws, plan.logits);
+  const double top_p = pa->select == BA_SELECT_TOPP ? (double)pa->top_p : 0.0;
+  const double *qv = q_var, *kv = k_var;
+  int comp = pa->comp == BA_COMP_DIAG ? 1 : 0;
   if (pa->comp == BA_COMP_EXACT) {  // NEXT-4: Delta = tr(SigmaQ SigmaK)/d (Eq. cov-comp)
     double *q_cov = at<double>(ws, plan.q_cov), *k_cov = at<double>(ws, plan.k_cov);
     BA_TRY(cuda_check(launch_block_cov(D.dtype, (int)D.d, q, prob->q_stride, D.b, D.hq, D.lq, (int)D.B,
@@ -272,16 +277,12 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
     BA_TRY(cuda_check(launch_block_cov(D.dtype, (int)D.d, k, prob->k_stride, D.b, D.hkv, D.lk, (int)D.B,
                                        sort_k(pa) ? sel->perm_k : nullptr, k_mean, k_cov, st), "block_cov(k)"));
     launches += 2;
-    BA_TRY(cuda_check(launch_scores((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, q_cov, k_mean, k_cov, 2,
-                                    (double)pa->beta, logits, st), "scores"));
-  } else {
-    BA_TRY(cuda_check(launch_scores((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, q_var, k_mean, k_var,
-                                    pa->comp == BA_COMP_DIAG ? 1 : 0, (double)pa->beta, logits, st), "scores"));
+    qv = q_cov; kv = k_cov; comp = 2;
   }
-  const double top_p = pa->select == BA_SELECT_TOPP ? (double)pa->top_p : 0.0;
-  BA_TRY(cuda_check(launch_topk(D.b * D.hq * D.nq, D.nk, D.kappa, top_p, logits, sel->kv_index, sel->kv_count,
-                                sel->mask, sel->block_prob, sel->threshold, st), "topk"));
-  launches += 2;
+  BA_TRY(cuda_check(launch_scores_topk((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, qv, k_mean, kv, comp,
+                                       (double)pa->beta, logits, D.kappa, top_p, sel->kv_index, sel->kv_count,
+                                       sel->mask, sel->block_prob, sel->threshold, st), "scores_topk"));
+  launches += 1;
   g_launches = launches;
   return BA_OK;
 }
@@ -575,6 +576,26 @@ ba_status ba_sparse_attn_peers(const ba_problem *prob, const ba_params *params, 
   a.out = out_peers[0];
   a.n_peers = n_peers;
   for (int p = 0; p < n_peers; ++p) a.out_peers[p] = out_peers[p];
+  for (int i = 0; i < 3; ++i) a.os[i] = prob->o_stride[i];
+  a.lse = lse;
+  return run_attn(a, stream);
+}
+
+ba_status ba_sparse_attn_multicast(const ba_problem *prob, const ba_params *params, const ba_selection *sel,
+                                   void *out_multicast, float *lse, cudaStream_t stream) {
+  g_err.clear();
+  BA_TRY(take_device_errors());
+  Dims D;
+  BA_TRY(check_problem(prob, params, &D));
+  BA_TRY(check_ptr("out_multicast", out_multicast));
+  if (!sel || !sel->q_sorted || !sel->k_sorted || !sel->v_sorted || !sel->kv_index || !sel->kv_count || !sel->perm_q)
+    return fail(BA_ERR_INVALID_ARGUMENT, "ba_sparse_attn_multicast reads the permuted copies, kv_index, kv_count, perm_q");
+  BA_TRY(check_strides("o", prob->o_stride, D.esz));
+  AttnArgs a = make_attn_sorted(D, params, sel);
+  if (!attn_sm100_supported(a))
+    return fail(BA_ERR_UNSUPPORTED, "multicast stores need the bf16 tcgen05 kernels (d = 128)");
+  a.out = out_multicast;
+  a.out_mc = out_multicast;
   for (int i = 0; i < 3; ++i) a.os[i] = prob->o_stride[i];
   a.lse = lse;
   return run_attn(a, stream);

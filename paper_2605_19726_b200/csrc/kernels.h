@@ -59,6 +59,7 @@ struct KeysArgs {
   int64_t batch;
 };
 size_t sort_ctrl_bytes(const SortGeom &g);
+// ctrl: sort_ctrl_bytes(g) of workspace, zeroed here by one memset per call.
 cudaError_t launch_keys_sort(const SortGeom &g, int dtype, int d, const KeysArgs &ka, uint32_t *keys_a,
                              uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, void *ctrl, cudaStream_t st,
                              int *launches);
@@ -93,6 +94,12 @@ cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t
 // largest N_k the top-kappa kernel takes: one warp holds a row of N_k fp64 logits (+1 KB of
 // histograms) in shared memory (227 KB per CTA)
 constexpr int64_t kSelectMaxNk = 28672;
+// K4a + K4b in one cooperative launch (grid-wide barrier between the score tiles and the
+// top-kappa rows); same arguments as launch_scores + launch_topk
+cudaError_t launch_scores_topk(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk,
+                               const double *q_mean, const double *q_var, const double *k_mean, const double *k_var,
+                               int comp, double beta, double *logits, int64_t kappa, double top_p, int32_t *kv_index,
+                               int32_t *kv_count, uint8_t *mask, double *prob, double *tau, cudaStream_t st);
 // top_p > 0: cumulative-mass budget (reading A23), kappa = the cap and the kv_index row stride
 cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *logits,
                         int32_t *kv_index, int32_t *kv_count, uint8_t *mask, double *prob,
@@ -126,6 +133,9 @@ struct AttnArgs {
   // as out) instead of out — the peers' symmetric buffers, pre-offset to this rank's heads
   int n_peers;
   void *out_peers[kMaxPeers];
+  // NVLS multicast (ba_sparse_attn_multicast): when set, every output row is stored once
+  // with multimem.st to this multicast address (same offsets / strides as out)
+  void *out_mc;
   // device-detected errors (two mapped host words, or nullptr): word kErrEmptyRow is
   // set when a query block's kv_count < 1 (its rows get O = 0, LSE = -inf), word
   // kErrBadIndex when a kv_index entry is outside [0, N_k) (the entry is skipped).

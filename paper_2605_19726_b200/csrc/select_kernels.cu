@@ -30,6 +30,10 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -337,6 +341,321 @@ cudaError_t launch_radix_sort(const SortGeom &g, uint32_t *keys_a, uint32_t *val
     uint32_t *tk = kin, *tv = vin;
     kin = kout; vin = vout; kout = tk; vout = tv;
   }
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// K1 + K2 in 1 + 4 launches ("onesweep", decoupled look-back):
+//   keys_hist_kernel   the norm keys of K1 (same arithmetic, reading A4) for every
+//                      sorted side, written to the key buffer, plus the per-segment
+//                      histograms of all four 8-bit digits (smem, flushed with one
+//                      atomic per non-zero bin);
+//   onesweep_kernel    one stable LSD pass per digit: a tile takes a ticket (tiles
+//                      therefore start in order), ranks its 4096 keys as before,
+//                      publishes its per-digit counts, sums its predecessors' counts
+//                      by looking back over their published (aggregate | inclusive)
+//                      words, and scatters through smem (coalesced runs).  The
+//                      segment's digit base comes from the histograms of the first
+//                      kernel, so no separate histogram / scan launches are needed.
+// Control block, zeroed by one memset per call (robust against any stale workspace
+// content): seg_hist [segs][4][256] u32, status [4][tiles][256] u64, tickets [4] u32.
+// =====================================================================================
+constexpr int kKeysRowsPerCta = 512;    // 16 half-warps x 32 rows
+constexpr int kKR = 8;                   // rows per half-warp in flight (8 x 16-byte loads per lane)
+constexpr uint64_t kStAgg = 1ull << 62, kStInc = 1ull << 63, kStVal = (1ull << 62) - 1;
+
+BA_DEVICE int64_t seg_of(const SortSide &sd, int64_t head, int64_t t) { return sd.seg_base + head * sd.n_win + t / sd.win; }
+BA_DEVICE uint32_t lane_id() { return threadIdx.x & 31u; }
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256, 3) keys_hist_kernel(SortGeom g, KeysArgs ka, float *__restrict__ keys,
+                                                        uint32_t *__restrict__ seg_hist) {
+  constexpr int PER_LANE = D / 16;
+  constexpr int BYTES = PER_LANE * (int)sizeof(T);
+  __shared__ uint32_t hist[2][4][256];  // the chunk's first two segments
+  __shared__ int64_t s_seg0;
+  // CTA -> (side, head row, chunk of kKeysRowsPerCta tokens)
+  int64_t c = blockIdx.x;
+  const int64_t chunks0 = g.side[0].heads * ((g.side[0].L + kKeysRowsPerCta - 1) / kKeysRowsPerCta);
+  const bool s1 = g.n_sides == 2 && c >= chunks0;
+  if (s1) c -= chunks0;
+  // the side's fields by value (a dynamically indexed kernel-parameter array goes to local memory)
+  SortSide sd;
+  sd.heads = s1 ? g.side[1].heads : g.side[0].heads;
+  sd.L = s1 ? g.side[1].L : g.side[0].L;
+  sd.win = s1 ? g.side[1].win : g.side[0].win;
+  sd.n_win = s1 ? g.side[1].n_win : g.side[0].n_win;
+  sd.base = s1 ? g.side[1].base : g.side[0].base;
+  sd.seg_base = s1 ? g.side[1].seg_base : g.side[0].seg_base;
+  const int64_t cph = (sd.L + kKeysRowsPerCta - 1) / kKeysRowsPerCta;
+  const int64_t head = c / cph, t0 = (c - head * cph) * kKeysRowsPerCta;
+  const int64_t nrow = imin64(kKeysRowsPerCta, sd.L - t0);
+  const T *x = static_cast<const T *>(s1 ? ka.x[1] : ka.x[0]);
+  const int64_t stv0 = s1 ? ka.st[1][0] : ka.st[0][0], stv1 = s1 ? ka.st[1][1] : ka.st[0][1],
+                stv2 = s1 ? ka.st[1][2] : ka.st[0][2];
+  float *user = s1 ? ka.user[1] : ka.user[0];
+  const int64_t H = sd.heads / ka.batch, bb = head / H, hh = head - bb * H;
+  for (int i = threadIdx.x; i < 2 * 4 * 256; i += 256) (&hist[0][0][0])[i] = 0u;
+  if (threadIdx.x == 0) s_seg0 = seg_of(sd, head, t0);
+  __syncthreads();
+  const int64_t seg0 = s_seg0;
+  const int lane16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
+  const T *xrow = x + bb * stv0 + hh * stv1 + lane16 * PER_LANE;
+  for (int it = 0; it < kKeysRowsPerCta / (16 * kKR); ++it) {
+    uint4 raw[kKR][BYTES > 16 ? 2 : 1];
+    int64_t rr[kKR];
+#pragma unroll
+    for (int k = 0; k < kKR; ++k) {  // every load first
+      const int64_t r = (int64_t)(it * 16 + hw) * kKR + k;
+      rr[k] = r;
+      if (r < nrow) {
+        const T *p = xrow + (t0 + r) * stv2;
+        if constexpr (BYTES == 8) {
+          const uint2 u = __ldg(reinterpret_cast<const uint2 *>(p));
+          raw[k][0] = make_uint4(u.x, u.y, 0, 0);
+        } else {
+          raw[k][0] = ldg16(p);
+          if constexpr (BYTES > 16) raw[k][BYTES > 16 ? 1 : 0] = ldg16(p + 16 / sizeof(T));
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kKR; ++k) {
+      float f[PER_LANE];
+      if constexpr (sizeof(T) == 2) {
+        const uint32_t w[4] = {raw[k][0].x, raw[k][0].y, raw[k][0].z, raw[k][0].w};
+#pragma unroll
+        for (int i = 0; i < PER_LANE / 2; ++i) {
+          f[2 * i] = __uint_as_float(w[i] << 16);
+          f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < PER_LANE; ++i) {
+          const uint4 &u = raw[k][i / 4];
+          const uint32_t w = (i & 3) == 0 ? u.x : (i & 3) == 1 ? u.y : (i & 3) == 2 ? u.z : u.w;
+          f[i] = __uint_as_float(w);
+        }
+      }
+      // IEEE fp32, product and sum each rounded (no FMA contraction): reading A4 (as K1)
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < PER_LANE; ++i) s = __fadd_rn(s, __fmul_rn(f[i], f[i]));
+      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 8));
+      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+      const bool ok = rr[k] < nrow;
+      const int64_t t = t0 + rr[k];
+      if (ok && lane16 == 0) {
+        keys[sd.base + head * sd.L + t] = s;
+        if (user) user[head * sd.L + t] = s;
+      }
+      // histograms: lanes 0-3 of each half-warp take one digit each; lanes with equal
+      // (segment, digit) are aggregated first (match_any) — the high digits of similar keys
+      // collide on a few bins, and same-address smem atomics would serialise
+      const int64_t sg = ok ? seg_of(sd, head, t) - seg0 : 0;
+      const uint32_t dg = (__float_as_uint(s) >> (8 * (lane16 & 3))) & 255u;
+      const bool act = ok && lane16 < 4;
+      const unsigned amask = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        const uint32_t tag = ((uint32_t)(lane16 & 3) << 8 | dg) + (sg < 2 ? (uint32_t)sg << 10 : 0x80000000u + lane_id());
+        const unsigned peers = __match_any_sync(amask, tag);
+        if ((peers & lanemask_lt()) == 0) {  // the lowest lane of each group adds the group's count
+          if (sg < 2) atomicAdd(&hist[sg][lane16 & 3][dg], (uint32_t)__popc(peers));
+          else atomicAdd(&seg_hist[(seg0 + sg) * 1024 + (lane16 & 3) * 256 + dg], 1u);  // tiny windows only
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t seg1 = seg_of(sd, head, t0 + nrow - 1);
+  for (int i = threadIdx.x; i < 2 * 1024; i += 256) {
+    const int sg = i >> 10;
+    if (seg0 + sg > seg1) break;
+    const uint32_t v = (&hist[sg][0][0])[i & 1023];
+    if (v) atomicAdd(&seg_hist[(seg0 + sg) * 1024 + (i & 1023)], v);
+  }
+}
+
+BA_DEVICE uint64_t ld_status(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+BA_DEVICE void st_status(uint64_t *p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// One stable LSD pass (digit `pass`) over every segment: see the block comment above.
+template <bool kFirst, bool kLast>
+__global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
+    SortGeom g, const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+    uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, const uint32_t *__restrict__ seg_hist,
+    uint64_t *__restrict__ status, uint32_t *__restrict__ tickets, int pass) {
+  constexpr int kWarps = kSortThreads / 32;
+  constexpr int kPerWarp = kSortTile / kWarps;  // 512
+  __shared__ uint32_t wcount[kWarps][256];
+  __shared__ uint32_t dstart[256];
+  __shared__ uint32_t s_off[256];
+  __shared__ uint32_t s_keys[kSortTile];
+  __shared__ uint32_t s_vals[kSortTile];
+  __shared__ uint32_t s_ticket;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(tickets + pass, 1u);  // tiles start in ticket order
+  __syncthreads();
+  const int64_t t = s_ticket;
+  const TileLoc loc = locate_tile(g, t);
+  if (loc.count <= 0) return;  // empty tail tile of a window: nobody looks back at it
+  const int shift = 8 * pass;
+  for (int i = threadIdx.x; i < kWarps * 256; i += kSortThreads) (&wcount[0][0])[i] = 0;
+  __syncthreads();
+
+  const int64_t base = loc.seg_start + loc.tile_off;
+  uint32_t key[kSortIPT], val[kSortIPT], rank[kSortIPT];
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r) {
+    const int item = warp * kPerWarp + r * 32 + lane;
+    const bool valid = item < loc.count;
+    key[r] = valid ? __ldg(keys_in + base + item) : 0xffffffffu;
+    if constexpr (kFirst) val[r] = (uint32_t)(loc.win_start + loc.tile_off + item);
+    else val[r] = valid ? __ldg(vals_in + base + item) : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r) {
+    const int item = warp * kPerWarp + r * 32 + lane;
+    const bool valid = item < loc.count;
+    const uint32_t digit = (key[r] >> shift) & 255u;
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    rank[r] = 0;
+    if (valid) {
+      const unsigned peers = __match_any_sync(vmask, digit);
+      const uint32_t before = wcount[warp][digit];
+      rank[r] = before + __popc(peers & lt);
+      __syncwarp(vmask);
+      if ((peers >> lane) == 1u) wcount[warp][digit] = before + __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  const int dg = threadIdx.x;  // one thread per digit from here
+  uint32_t cnt;
+  {  // per digit: exclusive over warps, then the tile's count
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = wcount[w][dg];
+      wcount[w][dg] = run;
+      run += c;
+    }
+    cnt = run;
+  }
+  // publish this tile's count, then look back over the segment's earlier tiles
+  uint64_t *st_pass = status + (int64_t)pass * g.tiles_total * 256;
+  const int64_t tile_in_seg = loc.tile_off / kSortTile;
+  uint64_t prefix = 0;
+  if (tile_in_seg == 0) {
+    st_status(st_pass + t * 256 + dg, kStInc | cnt);
+  } else {
+    st_status(st_pass + t * 256 + dg, kStAgg | cnt);
+    for (int64_t j = t - 1;; --j) {
+      uint64_t v;
+      do { v = ld_status(st_pass + j * 256 + dg); } while (!(v & (kStAgg | kStInc)));
+      prefix += v & kStVal;
+      if (v & kStInc) break;
+    }
+    st_status(st_pass + t * 256 + dg, kStInc | (prefix + cnt));
+  }
+  // the segment's digit base: exclusive scan of its histogram over the digits
+  dstart[dg] = seg_hist[loc.seg * 1024 + pass * 256 + dg];
+  __syncthreads();
+  {
+    const uint32_t v = dstart[dg];
+    for (int off = 1; off < 256; off <<= 1) {
+      __syncthreads();
+      const uint32_t a2 = dg >= off ? dstart[dg - off] : 0u;
+      __syncthreads();
+      dstart[dg] += a2;
+    }
+    __syncthreads();
+    s_off[dg] = dstart[dg] - v + (uint32_t)prefix;  // global position of this tile's first digit-dg item
+    __syncthreads();
+    dstart[dg] = cnt;  // reuse: tile counts -> tile-local digit starts
+  }
+  __syncthreads();
+  {
+    const uint32_t v = dstart[dg];
+    for (int off = 1; off < 256; off <<= 1) {
+      __syncthreads();
+      const uint32_t a2 = dg >= off ? dstart[dg - off] : 0u;
+      __syncthreads();
+      dstart[dg] += a2;
+    }
+    __syncthreads();
+    dstart[dg] -= v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSortIPT; ++r) {
+    const int item = warp * kPerWarp + r * 32 + lane;
+    if (item < loc.count) {
+      const uint32_t digit = (key[r] >> shift) & 255u;
+      const uint32_t pos = dstart[digit] + wcount[warp][digit] + rank[r];
+      s_keys[pos] = key[r];
+      s_vals[pos] = val[r];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < loc.count; i += kSortThreads) {
+    const uint32_t k = s_keys[i];
+    const uint32_t digit = (k >> shift) & 255u;
+    const int64_t gpos = s_off[digit] + (i - dstart[digit]);
+    if constexpr (kLast) {
+      const SortSide &sd = g.side[loc.side];
+      sd.perm_out[loc.head * sd.L + loc.win_start + gpos] = (int32_t)s_vals[i];
+    } else {
+      keys_out[loc.seg_start + gpos] = k;
+      vals_out[loc.seg_start + gpos] = s_vals[i];
+    }
+  }
+}
+
+size_t sort_ctrl_bytes(const SortGeom &g) {
+  return (size_t)g.segs_total * 1024 * 4 + (size_t)4 * g.tiles_total * 256 * 8 + 64;
+}
+
+cudaError_t launch_keys_sort(const SortGeom &g, int dtype, int d, const KeysArgs &ka, uint32_t *keys_a,
+                             uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, void *ctrl, cudaStream_t st,
+                             int *launches) {
+  if (g.tiles_total == 0) return cudaSuccess;
+  uint32_t *seg_hist = static_cast<uint32_t *>(ctrl);
+  uint64_t *status = reinterpret_cast<uint64_t *>(static_cast<char *>(ctrl) + (size_t)g.segs_total * 1024 * 4);
+  uint32_t *tickets = reinterpret_cast<uint32_t *>(status + (size_t)4 * g.tiles_total * 256);
+  cudaError_t e = cudaMemsetAsync(ctrl, 0, sort_ctrl_bytes(g), st);
+  if (e != cudaSuccess) return e;
+  int64_t ctas = 0;
+  for (int s = 0; s < g.n_sides; ++s) ctas += g.side[s].heads * ((g.side[s].L + kKeysRowsPerCta - 1) / kKeysRowsPerCta);
+#define BA_KH(T, D) \
+  keys_hist_kernel<T, D><<<(unsigned)ctas, 256, 0, st>>>(g, ka, reinterpret_cast<float *>(keys_a), seg_hist)
+  if (dtype == 0 && d == 128) BA_KH(__nv_bfloat16, 128);
+  else if (dtype == 0 && d == 64) BA_KH(__nv_bfloat16, 64);
+  else if (dtype == 1 && d == 128) BA_KH(float, 128);
+  else BA_KH(float, 64);
+#undef BA_KH
+  uint32_t *kin = keys_a, *vin = vals_a, *kout = keys_b, *vout = vals_b;
+  for (int pass = 0; pass < 4; ++pass) {
+    const unsigned grid = (unsigned)g.tiles_total;
+    if (pass == 0)
+      onesweep_kernel<true, false><<<grid, kSortThreads, 0, st>>>(g, kin, vin, kout, vout, seg_hist, status, tickets, pass);
+    else if (pass == 3)
+      onesweep_kernel<false, true><<<grid, kSortThreads, 0, st>>>(g, kin, vin, kout, vout, seg_hist, status, tickets, pass);
+    else
+      onesweep_kernel<false, false><<<grid, kSortThreads, 0, st>>>(g, kin, vin, kout, vout, seg_hist, status, tickets, pass);
+    uint32_t *tk = kin, *tv = vin;
+    kin = kout; vin = vout; kout = tk; vout = tv;
+  }
+  *launches += 6;  // memset + keys/histograms + 4 passes
   return cudaGetLastError();
 }
 
@@ -715,21 +1034,28 @@ constexpr int kScoresKS = 8;   // features per smem stage of the DMMA kernel (32
 // = one inner product of length d + d^2 with Xq = [Qbar/sqrt(d), (beta/d) vec SigmaQ] and
 // Xk = [Kbar, vec SigmaK] (the covariances are symmetric: tr(AB) = vec(A).vec(B));
 // q_var / k_var then point at the covariances [.., N, d, d].
-template <int D, int TILE, int KS, bool kExact = false>
-__global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_kernel(
-    int64_t hq, int64_t grp, int64_t nq, int64_t nk, const double *__restrict__ q_mean,
-    const double *__restrict__ q_var, const double *__restrict__ k_mean, const double *__restrict__ k_var,
-    int comp, double inv_sqrt_d, double beta_over_d, double *__restrict__ logits) {
+template <int TILE, int KS>
+struct ScoresSmem {
+  static constexpr int LDS = TILE + 8;  // k-row stride (doubles): 4 k-rows -> 2 wavefronts
+  double A[2][KS][LDS];
+  double B[2][KS][LDS];
+};
+
+// One TILE x TILE tile of l' (query blocks gq0.., key blocks gk0.. of q-head bhq) on the
+// FP64 tensor path; the CTA's (TILE/32)^2 warps, operands staged through sm.
+template <int D, int TILE, int KS, bool kExact>
+BA_DEVICE void scores_tile(int64_t hq, int64_t grp, int64_t nq, int64_t nk, const double *__restrict__ q_mean,
+                           const double *__restrict__ q_var, const double *__restrict__ k_mean,
+                           const double *__restrict__ k_var, int comp, double inv_sqrt_d, double beta_over_d,
+                           double *__restrict__ logits, int64_t bhq, int64_t gq0, int64_t gk0,
+                           ScoresSmem<TILE, KS> &sm) {
   constexpr int WARPS = (TILE / 32) * (TILE / 32), NT = WARPS * 32;
-  constexpr int LDS = TILE + 8;                       // k-row stride (doubles): 4 k-rows -> 2 wavefronts
   constexpr int LPT = TILE * KS / NT;               // features each thread loads per operand per stage
   constexpr int TPR = KS / LPT;                     // loader threads per row
-  __shared__ __align__(16) double As[2][KS][LDS];
-  __shared__ __align__(16) double Bs[2][KS][LDS];
-  const int64_t bhq = blockIdx.z;
+  auto &As = sm.A;
+  auto &Bs = sm.B;
   const int64_t b = bhq / hq, h = bhq - b * hq;
   const int64_t bhk = b * (hq / grp) + h / grp;
-  const int64_t gq0 = (int64_t)blockIdx.y * TILE, gk0 = (int64_t)blockIdx.x * TILE;
   constexpr int64_t VW = kExact ? D * D : D;  // per-block width of q_var / k_var
   const double *qm = q_mean + bhq * nq * D, *qv = q_var + bhq * nq * VW;
   const double *km = k_mean + bhk * nk * D, *kv = k_var + bhk * nk * VW;
@@ -820,6 +1146,16 @@ __global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_ker
       }
     }
   }
+}
+
+template <int D, int TILE, int KS, bool kExact = false>
+__global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_kernel(
+    int64_t hq, int64_t grp, int64_t nq, int64_t nk, const double *__restrict__ q_mean,
+    const double *__restrict__ q_var, const double *__restrict__ k_mean, const double *__restrict__ k_var,
+    int comp, double inv_sqrt_d, double beta_over_d, double *__restrict__ logits) {
+  __shared__ __align__(16) ScoresSmem<TILE, KS> sm;
+  scores_tile<D, TILE, KS, kExact>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, beta_over_d, logits,
+                                   blockIdx.z, (int64_t)blockIdx.y * TILE, (int64_t)blockIdx.x * TILE, sm);
 }
 
 cudaError_t launch_scores(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk,
@@ -944,16 +1280,11 @@ BA_DEVICE unsigned topp_count(const uint64_t *u, int64_t nk, double p, double to
   return c_gt + need;
 }
 
-__global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *__restrict__ logits,
-                            int32_t *__restrict__ kv_index, int32_t *__restrict__ kv_count,
-                            uint8_t *__restrict__ mask, double *__restrict__ prob,
-                            double *__restrict__ tau) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  unsigned *hist_base = reinterpret_cast<unsigned *>(smem_raw + (size_t)(blockDim.x >> 5) * nk * sizeof(double));
-  if (row >= rows) return;
-  double *x = reinterpret_cast<double *>(smem_raw) + (int64_t)warp * nk;
+// One row of K4b by one warp: x = the warp's nk doubles of smem, hist = its 256 counters.
+BA_DEVICE void topk_row(int64_t row, int64_t nk, int64_t kappa, double top_p, const double *__restrict__ logits,
+                        int32_t *__restrict__ kv_index, int32_t *__restrict__ kv_count, uint8_t *__restrict__ mask,
+                        double *__restrict__ prob, double *__restrict__ tau, double *x, unsigned *hist) {
+  const int lane = threadIdx.x & 31;
   const double *src = logits + row * nk;
   double mx = -INFINITY;
   for (int64_t j = lane; j < nk; j += 32) {
@@ -990,7 +1321,6 @@ __global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, double top_
     reinterpret_cast<uint64_t *>(x)[j] = ordered_bits(x[j]);  // in place: keys from here on
   __syncwarp();
   const uint64_t *u = reinterpret_cast<const uint64_t *>(x);
-  unsigned *hist = hist_base + warp * 256;
   uint64_t T = 0, pmask = 0;
   unsigned k_rem = (unsigned)kappa;  // TOPK: kappa; TOPP: min(kappa_row, kappa) (kappa = the density cap)
   if (topp) {
@@ -1062,6 +1392,90 @@ __global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, double top_
     const double tval = __longlong_as_double((long long)tb);
     tau[row] = topp ? tval : exp(tval - mx) / denom;
   }
+}
+
+__global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *__restrict__ logits,
+                            int32_t *__restrict__ kv_index, int32_t *__restrict__ kv_count,
+                            uint8_t *__restrict__ mask, double *__restrict__ prob,
+                            double *__restrict__ tau) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  unsigned *hist_base = reinterpret_cast<unsigned *>(smem_raw + (size_t)(blockDim.x >> 5) * nk * sizeof(double));
+  if (row >= rows) return;
+  topk_row(row, nk, kappa, top_p, logits, kv_index, kv_count, mask, prob, tau,
+           reinterpret_cast<double *>(smem_raw) + (int64_t)warp * nk, hist_base + warp * 256);
+}
+
+// K4a + K4b in ONE cooperative launch: every CTA first computes l' tiles (grid-strided over
+// the (key tile, query tile, q-head) space, 16 warps per 128 x 128 tile), the grid
+// synchronises once, and then every warp selects rows (grid-strided) — the top-kappa needs
+// complete rows, hence the grid-wide barrier.  Shared memory: the score tiles' operand
+// stages, reused by the top-kappa rows afterwards.
+template <int D, bool kExact>
+__global__ void __launch_bounds__(512, 1) scores_topk_kernel(int64_t hq, int64_t grp, int64_t nq, int64_t nk,
+                                                            const double *__restrict__ q_mean,
+                                                            const double *__restrict__ q_var,
+                                                            const double *__restrict__ k_mean,
+                                                            const double *__restrict__ k_var, int comp,
+                                                            double inv_sqrt_d, double beta_over_d,
+                                                            double *__restrict__ logits, int64_t bh_total,
+                                                            int64_t kappa, double top_p, int32_t *__restrict__ kv_index,
+                                                            int32_t *__restrict__ kv_count, uint8_t *__restrict__ mask,
+                                                            double *__restrict__ prob, double *__restrict__ tau,
+                                                            int topk_warps) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto &sm = *reinterpret_cast<ScoresSmem<128, kScoresKS> *>(smem_raw);
+  const int64_t tq = (nq + 127) / 128, tk = (nk + 127) / 128;
+  const int64_t tiles = tq * tk * bh_total;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t bhq = t / (tq * tk), r = t - bhq * tq * tk, iq = r / tk, ik = r - iq * tk;
+    scores_tile<D, 128, kScoresKS, kExact>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, beta_over_d,
+                                           logits, bhq, iq * 128, ik * 128, sm);
+    __syncthreads();  // the operand stages are reused by the next tile
+  }
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  const int warp = threadIdx.x >> 5;
+  if (warp >= topk_warps) return;
+  unsigned *hist_base = reinterpret_cast<unsigned *>(smem_raw + (size_t)topk_warps * nk * sizeof(double));
+  double *x = reinterpret_cast<double *>(smem_raw) + (int64_t)warp * nk;
+  const int64_t rows = bh_total * nq;
+  for (int64_t row = (int64_t)blockIdx.x * topk_warps + warp; row < rows; row += (int64_t)gridDim.x * topk_warps)
+    topk_row(row, nk, kappa, top_p, logits, kv_index, kv_count, mask, prob, tau, x, hist_base + warp * 256);
+}
+
+cudaError_t launch_scores_topk(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk,
+                               const double *q_mean, const double *q_var, const double *k_mean, const double *k_var,
+                               int comp, double beta, double *logits, int64_t kappa, double top_p, int32_t *kv_index,
+                               int32_t *kv_count, uint8_t *mask, double *prob, double *tau, cudaStream_t st) {
+  const double inv_sqrt_d = 1.0 / sqrt((double)d), bod = beta / (double)d;
+  int64_t grp = hq / hkv, bh_total = batch * hq;
+  constexpr size_t kMaxSmem = 227 * 1024;
+  const size_t per_warp = (size_t)nk * sizeof(double) + 256 * sizeof(unsigned);
+  int topk_warps = (int)std::min<size_t>(16, kMaxSmem / per_warp);
+  if (topk_warps < 1) return cudaErrorInvalidValue;  // N_k beyond the shared-memory row buffer (validated earlier)
+  size_t smem = std::max(sizeof(ScoresSmem<128, kScoresKS>), (size_t)topk_warps * per_warp);
+  void *kernel;
+  if (comp == 2) kernel = d == 128 ? (void *)scores_topk_kernel<128, true> : (void *)scores_topk_kernel<64, true>;
+  else kernel = d == 128 ? (void *)scores_topk_kernel<128, false> : (void *)scores_topk_kernel<64, false>;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0, dev = 0, sms = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 512, smem)) != cudaSuccess) return e;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+  const int64_t tiles = ((nq + 127) / 128) * ((nk + 127) / 128) * bh_total;
+  const int64_t rows_per_pass = (int64_t)topk_warps;
+  int64_t want = std::max<int64_t>(tiles, (bh_total * nq + rows_per_pass - 1) / rows_per_pass);
+  const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)per_sm * sms);
+  double kap_d = 0;
+  (void)kap_d;
+  void *args[] = {&hq, &grp, &nq, &nk, (void *)&q_mean, (void *)&q_var, (void *)&k_mean, (void *)&k_var, &comp,
+                  (void *)&inv_sqrt_d, (void *)&bod, &logits, &bh_total, &kappa, &top_p, &kv_index, &kv_count, &mask,
+                  &prob, &tau, &topk_warps};
+  return cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(512), args, smem, st);
 }
 
 cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *logits,

@@ -10,11 +10,18 @@
 
 namespace baatt {
 
-// Store one 16-byte vector of an output row to `out` (n_peers == 0) or to every peer
-// buffer at the same element offset (the fused head-parallel all-gather).
+// Store one 16-byte vector of an output row: to `out` (the plain case); to every peer
+// buffer at the same element offset (n_peers > 0: unicast NVLink stores, the fused
+// head-parallel all-gather); or ONCE to the NVLS multicast address out_mc (multimem.st:
+// the NVSwitch replicates the store into every device bound to the multicast object).
 template <typename T>
 BA_DEVICE void store_out_row16(const AttnArgs &a, int64_t elem_off, uint4 v) {
-  if (a.n_peers == 0) {
+  if (a.out_mc) {
+    T *p = static_cast<T *>(a.out_mc) + elem_off;
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(__uint_as_float(v.x)),
+                 "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+                 : "memory");
+  } else if (a.n_peers == 0) {
     *reinterpret_cast<uint4 *>(static_cast<T *>(a.out) + elem_off) = v;
   } else {
     for (int p = 0; p < a.n_peers; ++p) *reinterpret_cast<uint4 *>(static_cast<T *>(a.out_peers[p]) + elem_off) = v;

@@ -136,7 +136,9 @@ class FusedHeadGather:
     """Head-parallel output reassembly fused into the attention epilogue: the
     full O [b, Hq, L, d] lives in symmetric memory on every rank, and each
     rank's kernel stores its heads' rows into all ranks' copies over NVLink /
-    NVSwitch (ba_sparse_attn_peers); a symmetric-memory barrier then orders the
+    NVSwitch — once per row through the NVLS multicast address when the system
+    supports it (ba_sparse_attn_multicast, mc_ptr), else one unicast store per
+    peer (ba_sparse_attn_peers); a symmetric-memory barrier then orders the
     reads.  Replaces the NCCL all-gather of gather_heads."""
 
     def __init__(self, shape_full, dtype, device, q0: int, group=None):
@@ -147,6 +149,10 @@ class FusedHeadGather:
         self.full = symm_mem.empty(*shape_full, dtype=dtype, device=device)
         self.handle = symm_mem.rendezvous(self.full, group)
         self.peer_ptrs = peer_slice_ptrs(self.handle.buffer_ptrs, q0, self.full.stride(1), self.full.element_size())
+        # NVLS multicast address of the same buffer (0 when the NVSwitch / driver has no
+        # multicast support): one multimem.st reaches every rank's copy
+        mc = int(getattr(self.handle, "multicast_ptr", 0) or 0)
+        self.mc_ptr = peer_slice_ptrs([mc], q0, self.full.stride(1), self.full.element_size())[0] if mc else 0
 
     def barrier(self):
         self.handle.barrier()

@@ -619,13 +619,21 @@ ctx.sparse_attn_units(n // 3, n, f.peer_ptrs)
 f.barrier()
 torch.cuda.synchronize()
 ok2 = torch.equal(f.full, ref)
+mc = "unavailable"
+if f.mc_ptr:  # NVLS multicast stores (ba_sparse_attn_multicast), when the system supports multicast
+    f.full.fill_(float("nan"))
+    ctx.sparse_attn_multicast(f.mc_ptr)
+    f.barrier()
+    torch.cuda.synchronize()
+    mc = str(torch.equal(f.full, ref))
 dist.destroy_process_group()
-print("RESULT", ok1, ok2)
+print("MULTICAST", mc)
+print("RESULT", ok1, ok2, mc != "False")
 """)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
                         "--master-addr", "127.0.0.1", "--master-port", "29561", str(script)],
                        capture_output=True, text=True, timeout=300, cwd=root)
-    assert "RESULT True True" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "RESULT True True True" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
 
 
 # ---------------------------------------------------------------- boundary: S:393 empty rows, bad indices
