@@ -58,6 +58,10 @@ constexpr uint32_t Q_COL = 384;
 constexpr int kSoftmaxWarp0 = 2;
 constexpr int kThreads = 352;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef BA_PP_SPEC
+#define BA_PP_SPEC 0
+#endif
+constexpr bool kSpecMax = BA_PP_SPEC != 0;  // speculative row max (first P part against the running max)
 constexpr int kDefaultEmu = 0;             // pairs per 8 on the polynomial exp2 (off: MUFU + power cap wins)
 constexpr int kDefaultEmu64 = 1;           // dual-tile (B = 64) kernel
 constexpr int kMaskWords = 1024;           // bitmask capacity: N_k <= 32768 key blocks
@@ -408,8 +412,48 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
         }
       }
       if (lane == 0 && qd == 0) TR(6 + 5 * hf, j);
+      // p = 2^(s*c - m): FFMA2 for the argument, MUFU or polynomial exp2, FADD2 row sums
+      const uint64_t c2 = f2(c, c);
+      uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+      auto exp_pairs = [&](int i0, int i1, uint64_t nm2) {
+#pragma unroll
+        for (int i = i0; i < i1; ++i) {
+          const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
+          uint64_t p2;
+          if ((i & 7) < kEmu) {
+            p2 = exp2_poly2(x2);
+          } else {
+            float x0, x1;
+            unf2(x2, x0, x1);
+            p2 = f2(ex2(x0), ex2(x1));
+          }
+          acc2[i & 3] = fadd2(acc2[i & 3], p2);
+          float p0, p1;
+          unf2(p2, p0, p1);
+          sr[i] = pack_bf16(p0, p1);
+        }
+      };
+      constexpr int PP = HC / 4;  // packed pairs per P part (two parts per column half)
+      // Speculative max (as in the pair kernel): once the running max exists, the first P part
+      // is exponentiated against it while this half's max is reduced beside it, and the
+      // exchange with the other half follows; the part is redone if the max grew past the
+      // lazy-rescale threshold.  Iteration i reads S columns 4i..4i+3 and 2i, 2i+1, writes slot i.
+      const bool spec = kSpecMax && (PP == 16 || PP == 32) && mine && m != -INFINITY;
       float pmax = -INFINITY;
-      if (mine) {
+      if (spec) {
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        const uint64_t nm2 = f2(-m, -m);
+#pragma unroll
+        for (int i = 0; i < PP; ++i) {
+          constexpr int kCols = HC / PP;
+#pragma unroll
+          for (int t = 0; t < kCols; t += 2)
+            m4[((i & 1) << 1) + ((t >> 1) & 1)] =
+                fmax3(m4[((i & 1) << 1) + ((t >> 1) & 1)], __uint_as_float(sr[kCols * i + t]), __uint_as_float(sr[kCols * i + t + 1]));
+          exp_pairs(i, i + 1, nm2);
+        }
+        pmax = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      } else if (mine) {
         static_assert(HC % 16 == 0, "8 max chains");
         float m8[8];  // 8 independent FMNMX3 chains: latency, not issue, bounds the lone warp here
 #pragma unroll
@@ -450,6 +494,19 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
               tmem_st_x16(trow + O_COL + hf * 64 + q2 * 16, ov);
             }
             l *= corr;
+            if (spec) {  // redo the first part: its S columns [0, PP) were overwritten by P
+              if constexpr (PP == 32) tmem_ld_x32(trow + C::s_col(j & 1) + hf * HC, sr);
+              else if constexpr (PP == 16) tmem_ld_x16(trow + C::s_col(j & 1) + hf * HC, sr);
+              tmem_wait_ld();
+              if (kDual ? ragged_here : (last_ragged && j == cnt - 1)) {
+#pragma unroll
+                for (int i = 0; i < PP; ++i)
+                  if ((kDual ? i : hf * HC + i) >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
+              }
+#pragma unroll
+              for (int v = 0; v < 4; ++v) acc2[v] = 0ull;
+              exp_pairs(0, PP, f2(-m, -m));
+            }
           }
         }
       }
@@ -464,26 +521,10 @@ attn_sm100_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_k, co
         if (lane == 0) mbar_arrive(&bars.p_q[j & 1][hf][q]);
       };
       if (mine) {
-        // p = 2^(s*c - m): FFMA2 for the argument, MUFU or polynomial exp2, FADD2 row sums
-        const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
-        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-        for (int i = 0; i < HC / 2; ++i) {
-          if (i == HC / 4) publish(0);  // the first part's P goes out while the second is exponentiated
-          const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
-          uint64_t p2;
-          if ((i & 7) < kEmu) {
-            p2 = exp2_poly2(x2);
-          } else {
-            float x0, x1;
-            unf2(x2, x0, x1);
-            p2 = f2(ex2(x0), ex2(x1));
-          }
-          acc2[i & 3] = fadd2(acc2[i & 3], p2);
-          float p0, p1;
-          unf2(p2, p0, p1);
-          sr[i] = pack_bf16(p0, p1);
-        }
+        const uint64_t nm2 = f2(-m, -m);
+        if (!spec) exp_pairs(0, PP, nm2);
+        publish(0);  // the first part's P goes out while the second is exponentiated
+        exp_pairs(PP, 2 * PP, nm2);
         const uint64_t t2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
         float a0, a1;
         unf2(t2, a0, a1);

@@ -5,11 +5,14 @@
 // over its selected key blocks only, online softmax, rows
 // written back to pi_q(i).  Non-causal.
 //
-// A CTA owns the adjacent query blocks A = 2p and B = 2p+1 of one head (their
-// norm-sorted neighbourhoods select nearly the same key blocks: measured union
-// ratio 0.505-0.54) and walks the union of their index lists; every key/value
-// tile is loaded once for both.  Rows of a block that did not select the
-// current key block get P = 0.
+// A CTA owns the adjacent query blocks A = 2p and B = 2p+1 of one head and
+// walks their two index lists in lock step (PairWalk): first the key blocks
+// both selected (norm-sorted neighbours select nearly the same ones: the union
+// of the two lists is 1.01 kappa at A and C), each K/V tile loaded once for
+// both; then the blocks only A selected paired with the blocks only B selected,
+// two different tiles per step.  With equal list lengths (top-kappa) every step
+// is useful work for both blocks however incoherent the lists are; only an
+// unequal tail (top-p, kv_count) runs one block with P = 0.
 //
 // Why the pair: the lone MMA-issuing thread pays ~100 cycles per blocking
 // mbarrier wait that the shallow tcgen05 queue cannot hide (tools/mma_bench.cu
@@ -52,9 +55,10 @@ namespace pp {
 constexpr int BM = 128, BN = 128, HD = 128;
 constexpr uint32_t BOX = 128 * 64 * 2;       // 128 rows x 64 bf16 columns (16 KB)
 constexpr uint32_t TILE = 2 * BOX;           // 128 x 128 bf16 (32 KB)
-// K/V ring of 32 KB slots filled in the order K_0, V_0, K_1, V_1, ...; a slot is
-// released by a commit after its last reader (K_u after S_B(u), V_u after
-// PV_B(u)), which is also the fill order, so 5 slots keep ~2 tiles in flight.
+// K/V ring of 32 KB slots filled in the MMA's consumption order: per step u a
+// shared tile is K_u, V_u; a split step K_A(u), K_B(u), V_A(u), V_B(u).  A slot is
+// released by a commit after its last reader (shared K_u after S_B(u), V_u after
+// PV_B(u); split: each after its one reader), so 5 slots keep 1-2 steps in flight.
 constexpr int NSLOT = 5;
 BA_DEVICE constexpr uint32_t s_col(int x) { return x ? 128u : 0u; }
 constexpr uint32_t O_COL0 = 256;
@@ -66,6 +70,10 @@ constexpr int kPSplit = BA_PP_PSPLIT;     // P handed to the MMA in this many ke
 constexpr int kThreads = 384;             // 12 warps: 8 softmax (warpgroups 0, 1) + warpgroup 2 (producer, MMA, 2 idle)
 constexpr int kRegsSoftmax = 208, kRegsSide = 80;  // setmaxnreg: 8*32*208 + 4*32*80 = 63488 <= 65536
 constexpr float kRescaleThreshold = 8.0f;
+#ifndef BA_PP_SPEC
+#define BA_PP_SPEC 0
+#endif
+constexpr bool kSpecMax = BA_PP_SPEC != 0;  // speculative row max (first P part against the running max)
 constexpr int kMaskWords = 256;                             // nk <= 8192 (L <= 1M tokens)
 constexpr int kTraceTiles = 8;
 constexpr int kDefaultEmu = 1;  // 1 of 8 exp2 pairs on the FMA pipe: +2.4% at A, +1.4% at C (EMU sweep, profiles/round1_microbench.txt)
@@ -86,21 +94,62 @@ struct __align__(8) Bars {
   uint64_t s_full[2], p_part[2][kPSplit];    // per query block (A, B); p_part[q]: P of key part q in TMEM
   uint64_t o_final;
   uint32_t tmem_base;
-  uint32_t n_union;
-  uint32_t last_ragged;
+  uint32_t n_common, n_only_a, n_only_b;  // |S_A & S_B|, |S_A \ S_B|, |S_B \ S_A|
 };
 static_assert(sizeof(Bars) <= 256, "barrier block");
 
-struct UnionWalk {
+// Ascending walk over the set bits of one of S_A & S_B (kind 0), S_A \ S_B (1), S_B \ S_A (2).
+struct BitWalk {
   const uint32_t *ma, *mb;
-  int w;
+  int w, kind;
   uint32_t rem;
-  BA_DEVICE void init(const uint32_t *a_, const uint32_t *b_) { ma = a_; mb = b_; w = 0; rem = a_[0] | b_[0]; }
+  BA_DEVICE uint32_t word(int i) const {
+    return kind == 0 ? (ma[i] & mb[i]) : kind == 1 ? (ma[i] & ~mb[i]) : (mb[i] & ~ma[i]);
+  }
+  BA_DEVICE void init(const uint32_t *a_, const uint32_t *b_, int k) { ma = a_; mb = b_; kind = k; w = 0; rem = word(0); }
   BA_DEVICE int next() {
-    while (rem == 0) { ++w; rem = ma[w] | mb[w]; }
+    while (rem == 0) rem = word(++w);
     const int bit = __ffs(rem) - 1;
     rem &= rem - 1;
     return w * 32 + bit;
+  }
+};
+
+// One step of the pair: key block ta for block A, tb for block B.  ta == tb: one
+// shared K/V tile (2 ring items); ta != tb: two tiles (4 items).  mine_x = 0: block x
+// has no key block left at this step and runs the other's tile with P = 0.
+struct Step {
+  int ta, tb;
+  bool mine_a, mine_b;
+  BA_DEVICE bool split() const { return ta != tb; }
+  BA_DEVICE int items() const { return ta != tb ? 4 : 2; }
+};
+
+// The step sequence every role enumerates identically: the common blocks in
+// ascending order, then the i-th block only A selected with the i-th only B
+// selected.  n_steps = n_common + max(n_only_a, n_only_b).
+struct PairWalk {
+  BitWalk c, xa, xb;
+  int u, nc, na, nb;
+  BA_DEVICE void init(const uint32_t *ma, const uint32_t *mb, int nc_, int na_, int nb_) {
+    c.init(ma, mb, 0); xa.init(ma, mb, 1); xb.init(ma, mb, 2);
+    u = 0; nc = nc_; na = na_; nb = nb_;
+  }
+  BA_DEVICE Step next() {
+    Step s;
+    if (u < nc) {
+      s.ta = s.tb = c.next();
+      s.mine_a = s.mine_b = true;
+    } else {
+      const int i = u - nc;
+      s.mine_a = i < na;
+      s.mine_b = i < nb;
+      const int ta = s.mine_a ? xa.next() : -1, tb = s.mine_b ? xb.next() : -1;
+      s.ta = s.mine_a ? ta : tb;
+      s.tb = s.mine_b ? tb : ta;
+    }
+    ++u;
+    return s;
   }
 };
 
@@ -163,14 +212,19 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
   }
   __syncthreads();
   if (warp == 0) {
-    unsigned c = 0;
-    for (int w = lane; w < nw; w += 32) c += __popc(mask_a[w] | mask_b[w]);
-    c = __reduce_add_sync(0xffffffffu, c);
+    unsigned cc = 0, ca = 0, cb = 0;
+    for (int w = lane; w < nw; w += 32) {
+      cc += __popc(mask_a[w] & mask_b[w]);
+      ca += __popc(mask_a[w] & ~mask_b[w]);
+      cb += __popc(mask_b[w] & ~mask_a[w]);
+    }
+    cc = __reduce_add_sync(0xffffffffu, cc);
+    ca = __reduce_add_sync(0xffffffffu, ca);
+    cb = __reduce_add_sync(0xffffffffu, cb);
     if (lane == 0) {
-      bars.n_union = c;
-      const int64_t gl = a.nk - 1;
-      const bool sel_last = ((mask_a[gl >> 5] | mask_b[gl >> 5]) >> (gl & 31)) & 1u;
-      bars.last_ragged = sel_last && (a.lk - gl * (int64_t)BN) < BN;
+      bars.n_common = cc;
+      bars.n_only_a = ca;
+      bars.n_only_b = cb;
       mbar_init(&bars.q_full, 1);
       for (int s = 0; s < NSLOT; ++s) { mbar_init(&bars.full[s], 1); mbar_init(&bars.empty[s], 1); }
       for (int s = 0; s < 2; ++s) {
@@ -192,7 +246,8 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
-  const int cnt = (int)bars.n_union;
+  const int n_common = (int)bars.n_common, n_only_a = (int)bars.n_only_a, n_only_b = (int)bars.n_only_b;
+  const int cnt = n_common + imax(n_only_a, n_only_b);  // steps
 
   if (warp >= 8) {
   // warpgroup 2 gives registers to the softmax warpgroups (each softmax thread holds a
@@ -228,45 +283,57 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
           tma_load_4d(dq + BOX, &tm_q, &bars.q_full, 64, (int)((ga + q2) * BM), (int)h, (int)b);
         }
       }
+      // ring items of a step in consumption order: shared K, V; split K_A, K_B, V_A, V_B
       if constexpr (kGather & 2) {
-        UnionWalk walk;
-        walk.init(mask_a, mask_b);
+        PairWalk walk;
+        walk.init(mask_a, mask_b, n_common, n_only_a, n_only_b);
+        int j = 0;
         for (int u = 0; u < cnt; ++u) {
-          const int gk = walk.next();
-          int rr[4];  // the ragged tail repeats the last key row (its columns are masked to -inf)
+          const Step st = walk.next();
+          const int nt = st.split() ? 2 : 1;
+          int rr[2][4];  // the ragged tail repeats the last key row (its columns are masked to -inf)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int64_t tok = imin64((int64_t)gk * BN + 4 * lane + i, a.lk - 1);
-            rr[i] = (int)(kb + __ldg(a.perm_k + kb + tok));
+          for (int t = 0; t < 2; ++t) {
+            const int gk = t ? st.tb : st.ta;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int64_t tok = imin64((int64_t)gk * BN + 4 * lane + i, a.lk - 1);
+              rr[t][i] = (t < nt) ? (int)(kb + __ldg(a.perm_k + kb + tok)) : 0;
+            }
           }
-#pragma unroll
-          for (int kv = 0; kv < 2; ++kv) {  // item j = 2u + kv: K_u then V_u
-            const int j = 2 * u + kv, s = j % kSlots;
-            mbar_wait(&bars.empty[s], ((uint32_t)(j / kSlots) & 1u) ^ 1u);
-            if (kv == 0 && lane == 0) TR(0, u);
-            if (lane == 0) mbar_expect_tx(&bars.full[s], TILE);
-            __syncwarp();
-            const uint32_t dst = base + SMEM_SLOT + s * TILE + lane * 512;
-            const CUtensorMap *map = kv ? &tm_v : &tm_k;
-            tma_gather4(dst, map, &bars.full[s], 0, rr[0], rr[1], rr[2], rr[3]);
-            tma_gather4(dst + BOX, map, &bars.full[s], 64, rr[0], rr[1], rr[2], rr[3]);
+          for (int kv = 0; kv < 2; ++kv) {
+            for (int t = 0; t < nt; ++t, ++j) {
+              const int s = j % kSlots;
+              mbar_wait(&bars.empty[s], ((uint32_t)(j / kSlots) & 1u) ^ 1u);
+              if (kv == 0 && t == 0 && lane == 0) TR(0, u);
+              if (lane == 0) mbar_expect_tx(&bars.full[s], TILE);
+              __syncwarp();
+              const uint32_t dst = base + SMEM_SLOT + s * TILE + lane * 512;
+              const CUtensorMap *map = kv ? &tm_v : &tm_k;
+              const int *r4 = rr[t];
+              tma_gather4(dst, map, &bars.full[s], 0, r4[0], r4[1], r4[2], r4[3]);
+              tma_gather4(dst + BOX, map, &bars.full[s], 64, r4[0], r4[1], r4[2], r4[3]);
+            }
           }
         }
       } else if (lane == 0) {
-        UnionWalk walk;
-        walk.init(mask_a, mask_b);
+        PairWalk walk;
+        walk.init(mask_a, mask_b, n_common, n_only_a, n_only_b);
+        int j = 0;
         for (int u = 0; u < cnt; ++u) {
-          const int gk = walk.next();
-#pragma unroll
-          for (int kv = 0; kv < 2; ++kv) {  // item j = 2u + kv: K_u then V_u
-            const int j = 2 * u + kv, s = j % kSlots;
-            mbar_wait(&bars.empty[s], ((uint32_t)(j / kSlots) & 1u) ^ 1u);
-            if (kv == 0) TR(0, u);
-            const uint32_t dst = base + SMEM_SLOT + s * TILE;
-            const CUtensorMap *map = kv ? &tm_v : &tm_k;
-            mbar_expect_tx(&bars.full[s], TILE);
-            tma_load_4d(dst, map, &bars.full[s], 0, gk * BN, (int)hk, (int)b);
-            tma_load_4d(dst + BOX, map, &bars.full[s], 64, gk * BN, (int)hk, (int)b);
+          const Step st = walk.next();
+          const int nt = st.split() ? 2 : 1;
+          for (int kv = 0; kv < 2; ++kv) {
+            for (int t = 0; t < nt; ++t, ++j) {
+              const int s = j % kSlots, gk = t ? st.tb : st.ta;
+              mbar_wait(&bars.empty[s], ((uint32_t)(j / kSlots) & 1u) ^ 1u);
+              if (kv == 0 && t == 0) TR(0, u);
+              const uint32_t dst = base + SMEM_SLOT + s * TILE;
+              const CUtensorMap *map = kv ? &tm_v : &tm_k;
+              mbar_expect_tx(&bars.full[s], TILE);
+              tma_load_4d(dst, map, &bars.full[s], 0, gk * BN, (int)hk, (int)b);
+              tma_load_4d(dst + BOX, map, &bars.full[s], 64, gk * BN, (int)hk, (int)b);
+            }
           }
         }
       }
@@ -281,10 +348,10 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         mbar_wait(&bars.full[j % kSlots], (uint32_t)(j / kSlots) & 1u);
         tc_fence_after();
       };
-      auto issue_s = [&](int x, int u) {  // S_x = Q_x K_u^T into S_x's TMEM columns
+      auto issue_s = [&](int x, int jk) {  // S_x = Q_x K^T, K in ring item jk, into S_x's TMEM columns
         // descriptors built once per tile; the K-step offsets are added to the start-address
         // field (addr >> 4, 14 bits: every smem address here is < 256 KB, so no carry out)
-        const uint64_t dq = make_desc(base + SMEM_Q + x * TILE, 16, 1024), dk = make_desc(slot_addr(2 * u), 16, 1024);
+        const uint64_t dq = make_desc(base + SMEM_Q + x * TILE, 16, 1024), dk = make_desc(slot_addr(jk), 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint64_t off = ((kk >> 2) * BOX + (kk & 3) * 32) >> 4;
@@ -292,49 +359,69 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         }
         mma_commit(&bars.s_full[x]);
       };
-      // O_x += P_x V_u, P_x read from TMEM, in two halves of 64 keys: the first half is issued
-      // as soon as the softmax has stored P for keys 0-63 (p_half), overlapping its second half
-      auto issue_pv = [&](int x, int u, int h) {
-        const uint64_t dv = make_desc(slot_addr(2 * u + 1), BOX, 1024);
+      // O_x += P_x V, V in ring item jv, P_x read from TMEM, in kPSplit parts of keys: each part is
+      // issued as soon as the softmax has stored its P, overlapping the exps of the next part
+      auto issue_pv = [&](int x, int u, int jv, int h) {
+        const uint64_t dv = make_desc(slot_addr(jv), BOX, 1024);
         constexpr int KPP = BN / 16 / kPSplit;  // 16-key MMA steps per part
 #pragma unroll
         for (int kk = KPP * h; kk < KPP * h + KPP; ++kk)
           mma_ts(tmem + O_COL0 + 128 * x, tmem + s_col(x) + kk * 8, dv + (uint64_t)((kk * 2048) >> 4), IDESC_O,
                  (u > 0 || kk > 0) ? 1u : 0u);
       };
-      wait_full(0);
-      issue_s(0, 0);
-      issue_s(1, 0);
-      mma_commit(&bars.empty[0]);  // K_0 read by both
+      // ring items of a step starting at item j: K_A, K_B, V_A, V_B
+      auto k_item = [](const Step &st, int j, int x) { return j + (st.split() ? x : 0); };
+      auto v_item = [](const Step &st, int j, int x) { return j + (st.split() ? 2 + x : 1); };
+      PairWalk walk;
+      walk.init(mask_a, mask_b, n_common, n_only_a, n_only_b);
+      Step cur = walk.next();
+      int jc = 0;
+      wait_full(k_item(cur, jc, 0));
+      issue_s(0, k_item(cur, jc, 0));
+      if (cur.split()) {
+        mma_commit(&bars.empty[k_item(cur, jc, 0) % kSlots]);  // K_A(0): its one reader issued
+        wait_full(k_item(cur, jc, 1));
+      }
+      issue_s(1, k_item(cur, jc, 1));
+      mma_commit(&bars.empty[k_item(cur, jc, 1) % kSlots]);  // K_0 (or K_B(0)): every reader issued
       for (int u = 0; u < cnt; ++u) {
         const bool next = u + 1 < cnt;
+        const int jn = jc + cur.items();
+        Step nx = cur;
+        if (next) nx = walk.next();
         mbar_wait(&bars.p_part[0][0], (uint32_t)u & 1u);  // softmax A wrote P_A(u), first key part
         TR(1, u);
-        wait_full(2 * u + 1);
-        issue_pv(0, u, 0);
+        wait_full(v_item(cur, jc, 0));
+        issue_pv(0, u, v_item(cur, jc, 0), 0);
 #pragma unroll
         for (int q = 1; q < kPSplit; ++q) {
           mbar_wait(&bars.p_part[0][q], (uint32_t)u & 1u);
           tc_fence_after();
-          issue_pv(0, u, q);
+          issue_pv(0, u, v_item(cur, jc, 0), q);
         }
+        if (cur.split()) mma_commit(&bars.empty[v_item(cur, jc, 0) % kSlots]);  // V_A(u)
         if (next) {
-          wait_full(2 * u + 2);
-          issue_s(0, u + 1);  // S_A buffer reuse: after PV_A(u) in issue order
+          wait_full(k_item(nx, jn, 0));
+          issue_s(0, k_item(nx, jn, 0));  // S_A buffer reuse: after PV_A(u) in issue order
+          if (nx.split()) mma_commit(&bars.empty[k_item(nx, jn, 0) % kSlots]);  // K_A(u+1)
           TR(2, u + 1);
         }
+        if (cur.split()) wait_full(v_item(cur, jc, 1));
 #pragma unroll
         for (int q = 0; q < kPSplit; ++q) {
           mbar_wait(&bars.p_part[1][q], (uint32_t)u & 1u);  // softmax B wrote P_B(u), key part q
           if (q == 0) TR(3, u);
           tc_fence_after();
-          issue_pv(1, u, q);
+          issue_pv(1, u, v_item(cur, jc, 1), q);
         }
-        mma_commit(&bars.empty[(2 * u + 1) % kSlots]);  // V_u: both readers issued
+        mma_commit(&bars.empty[v_item(cur, jc, 1) % kSlots]);  // V_u (or V_B(u)): every reader issued
         if (next) {
-          issue_s(1, u + 1);
-          mma_commit(&bars.empty[(2 * u + 2) % kSlots]);  // K_{u+1}: both readers issued
+          if (nx.split()) wait_full(k_item(nx, jn, 1));
+          issue_s(1, k_item(nx, jn, 1));
+          mma_commit(&bars.empty[k_item(nx, jn, 1) % kSlots]);  // K_{u+1} (or K_B(u+1)): every reader issued
         }
+        cur = nx;
+        jc = jn;
       }
       mma_commit(&bars.o_final);
     }
@@ -350,14 +437,21 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     const uint32_t scol = s_col(x), ocol = O_COL0 + 128 * x;
     const int64_t row0 = (ga + x) * (int64_t)BM;
     const int nrows = (int)imin64(BM, a.lq - row0);
-    const uint32_t *my_mask = x ? mask_b : mask_a;
-    const bool last_ragged = bars.last_ragged != 0u;
-    const int64_t ragged_valid = a.lk - (a.nk - 1) * (int64_t)BN;
+    const int64_t ragged_valid = a.lk - (a.nk - 1) * (int64_t)BN;  // < BN: the last key block is ragged
+    // PairWalk order, without walking: block x has a key block at steps u < n_common + n_only_x, and
+    // the ascending walks meet the largest block N_k - 1 last (of the common blocks, or of x's own)
+    const int my_only = x ? n_only_b : n_only_a;
+    const int n_mine = n_common + my_only;
+    int ragged_step = -1;
+    if (ragged_valid < BN) {
+      const int gl = (int)(a.nk - 1);
+      const bool in_a = (mask_a[gl >> 5] >> (gl & 31)) & 1u, in_b = (mask_b[gl >> 5] >> (gl & 31)) & 1u;
+      if (in_a && in_b) ragged_step = n_common - 1;
+      else if (x ? in_b : in_a) ragged_step = n_mine - 1;
+    }
     const float c = a.scale * 1.4426950408889634f;
     float m = -INFINITY, l = 0.f;
     uint32_t sr[128];
-    UnionWalk walk;
-    walk.init(mask_a, mask_b);
     // P (bf16 pairs) over S in TMEM: part q = keys 128q/kPSplit .. -> columns 64q/kPSplit ..
     // (S of those columns is already in registers), then p_part[q]
     auto publish_part = [&](int q) {
@@ -370,8 +464,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       if (lane == 0) mbar_arrive(&bars.p_part[x][q]);
     };
     for (int u = 0; u < cnt; ++u) {
-      const int gk = walk.next();
-      const bool mine = (my_mask[gk >> 5] >> (gk & 31)) & 1u;  // warpgroup-uniform
+      const bool mine = u < n_mine;  // warpgroup-uniform
       const bool trx = kTrace && (warp == 0 || warp == 4) && lane == 0;
       mbar_wait(&bars.s_full[x], (uint32_t)u & 1u);
       if (trx) TR(4 + 4 * x, u);
@@ -385,24 +478,52 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         for (int q4 = 0; q4 < 4; ++q4) tmem_ld_x32(trow + scol + q4 * 32, sr + q4 * 32);
         tmem_wait_ld();
         if (trx) TR(5 + 4 * x, u);
-        if (last_ragged && u == cnt - 1) {
+        if (u == ragged_step) {
 #pragma unroll
           for (int i = 0; i < 128; ++i)
             if (i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
         }
-        // row max: 8 independent FMNMX3 chains of depth 8 (the lone warp's latency, not its issue, bounds this)
-        float m8[8];
+        const uint64_t c2 = f2(c, c);
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+        // exp2 of key pairs [i0, i1) against the running max m: packed bf16 P into sr[i], sums into acc2
+        auto exp_pairs = [&](int i0, int i1, uint64_t nm2) {
 #pragma unroll
-        for (int v = 0; v < 8; ++v) m8[v] = fmaxf(__uint_as_float(sr[2 * v]), __uint_as_float(sr[2 * v + 1]));
+          for (int i = i0; i < i1; ++i) {
+            const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
+            uint64_t p2;
+            if ((i & 7) < kEmu) {
+              p2 = exp2_poly2(x2);
+            } else {
+              float x0, x1;
+              unf2(x2, x0, x1);
+              p2 = f2(ex2(x0), ex2(x1));
+            }
+            acc2[i & 3] = fadd2(acc2[i & 3], p2);
+            float p0, p1;
+            unf2(p2, p0, p1);
+            sr[i] = pack_bf16(p0, p1);
+          }
+        };
+        constexpr int PP = 64 / kPSplit;  // packed pairs per P part
+        if (kSpecMax && m != -INFINITY) {
+          // Speculative max: the first P part is exponentiated against the running max m while the
+          // tile's row max is reduced beside it (independent FMNMX3 chains fill the MUFU issue gaps
+          // instead of preceding the exps).  Exact unless the max grew by more than the lazy-rescale
+          // threshold (P <= 2^8 otherwise, as in the non-speculative path); then the part is redone.
+          // Iteration i reads S columns 4i..4i+3 (max) and 2i, 2i+1 (exp) and writes slot i <= 2i.
+          float m4[4];
 #pragma unroll
-        for (int i = 16; i < 128; i += 16) {
+          for (int v = 0; v < 4; ++v) m4[v] = -INFINITY;
+          const uint64_t nm2 = f2(-m, -m);
 #pragma unroll
-          for (int v = 0; v < 8; ++v) m8[v] = fmax3(m8[v], __uint_as_float(sr[i + 2 * v]), __uint_as_float(sr[i + 2 * v + 1]));
-        }
-        const float mt = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7])) * c;
-        if (m == -INFINITY) {
-          m = mt;  // first tile of these rows: O rows are still zero (earlier P rows were 0)
-        } else {
+          for (int i = 0; i < PP; ++i) {
+            constexpr int kCols = 128 / PP;  // max columns per exp pair
+#pragma unroll
+            for (int t = 0; t < kCols; t += 2)
+              m4[((i & 1) << 1) + ((t >> 1) & 1)] = fmax3(m4[((i & 1) << 1) + ((t >> 1) & 1)], __uint_as_float(sr[kCols * i + t]), __uint_as_float(sr[kCols * i + t + 1]));
+            exp_pairs(i, i + 1, nm2);
+          }
+          const float mt = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * c;
           const bool need = mt > m + kRescaleThreshold;
           if (__any_sync(0xffffffffu, need)) {
             // PV_x(u-1) is complete: the commit behind s_full[x](u) tracks every earlier MMA
@@ -418,29 +539,56 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
               tmem_st_x16(trow + ocol + q8 * 16, ov);
             }
             l *= corr;
-          }
-        }
-        const uint64_t c2 = f2(c, c), nm2 = f2(-m, -m);
-        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+            // redo the first part: its S columns [0, PP) were overwritten by P (S is intact in TMEM)
+            if constexpr (PP == 32) tmem_ld_x32(trow + scol, sr);
+            else tmem_ld_x16(trow + scol, sr);
+            tmem_wait_ld();
+            if (u == ragged_step) {
 #pragma unroll
-        for (int h2 = 0; h2 < kPSplit; ++h2) {  // key parts in order; each part's P goes out as soon as done
-          constexpr int PP = 64 / kPSplit;       // packed pairs per part
-#pragma unroll
-          for (int i = PP * h2; i < PP * h2 + PP; ++i) {
-            const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
-            uint64_t p2;
-            if ((i & 7) < kEmu) {
-              p2 = exp2_poly2(x2);
-            } else {
-              float x0, x1;
-              unf2(x2, x0, x1);
-              p2 = f2(ex2(x0), ex2(x1));
+              for (int i = 0; i < PP; ++i)
+                if (i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
             }
-            acc2[i & 3] = fadd2(acc2[i & 3], p2);
-            float p0, p1;
-            unf2(p2, p0, p1);
-            sr[i] = pack_bf16(p0, p1);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc2[v] = 0ull;
+            exp_pairs(0, PP, f2(-m, -m));
           }
+        } else {
+          // row max: 8 independent FMNMX3 chains of depth 8 (the lone warp's latency, not its issue, bounds this)
+          float m8[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) m8[v] = fmaxf(__uint_as_float(sr[2 * v]), __uint_as_float(sr[2 * v + 1]));
+#pragma unroll
+          for (int i = 16; i < 128; i += 16) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v) m8[v] = fmax3(m8[v], __uint_as_float(sr[i + 2 * v]), __uint_as_float(sr[i + 2 * v + 1]));
+          }
+          const float mt = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7])) * c;
+          if (m == -INFINITY) {
+            m = mt;  // first tile of these rows: O rows are still zero (earlier P rows were 0)
+          } else {
+            const bool need = mt > m + kRescaleThreshold;
+            if (__any_sync(0xffffffffu, need)) {
+              float corr = 1.f;
+              if (need) { corr = ex2(m - mt); m = mt; }
+              uint32_t ov[16];
+#pragma unroll
+              for (int q8 = 0; q8 < 8; ++q8) {
+                tmem_ld_x16(trow + ocol + q8 * 16, ov);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
+                tmem_st_x16(trow + ocol + q8 * 16, ov);
+              }
+              l *= corr;
+            }
+          }
+          exp_pairs(0, PP, f2(-m, -m));
+        }
+        publish_part(0);
+        const uint64_t nm2 = f2(-m, -m);
+#pragma unroll
+        for (int h2 = 1; h2 < kPSplit; ++h2) {  // remaining key parts in order; each part's P goes out as soon as done
+          exp_pairs(PP * h2, PP * h2 + PP, nm2);
           if (h2 < kPSplit - 1) publish_part(h2);
         }
         const uint64_t t2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));

@@ -32,6 +32,7 @@ template <> struct Chunk<__nv_bfloat16> {
 };
 
 BA_DEVICE int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+BA_DEVICE int imax(int a, int b) { return a > b ? a : b; }
 
 BA_DEVICE uint4 ldg16(const void *p) { return __ldg(reinterpret_cast<const uint4 *>(p)); }
 BA_DEVICE void stg16(void *p, const uint4 &v) { *reinterpret_cast<uint4 *>(p) = v; }

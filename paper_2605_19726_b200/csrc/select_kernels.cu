@@ -399,6 +399,11 @@ __global__ void __launch_bounds__(256, 3) keys_hist_kernel(SortGeom g, KeysArgs 
   if (threadIdx.x == 0) s_seg0 = seg_of(sd, head, t0);
   __syncthreads();
   const int64_t seg0 = s_seg0;
+  // segment of row t relative to seg0 without a per-row 64-bit division: a chunk spans at
+  // most two windows of >= kKeysRowsPerCta tokens (boundary b1); tiny windows divide in 32 bits
+  const int64_t w0 = t0 / sd.win, b1 = (w0 + 1) * sd.win;
+  const bool tiny_win = sd.win < kKeysRowsPerCta;
+  const uint32_t win32 = (uint32_t)imin64(sd.win, 0x7fffffff);
   const int lane16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
   const T *xrow = x + bb * stv0 + hh * stv1 + lane16 * PER_LANE;
   for (int it = 0; it < kKeysRowsPerCta / (16 * kKR); ++it) {
@@ -454,7 +459,7 @@ __global__ void __launch_bounds__(256, 3) keys_hist_kernel(SortGeom g, KeysArgs 
       // histograms: lanes 0-3 of each half-warp take one digit each; lanes with equal
       // (segment, digit) are aggregated first (match_any) — the high digits of similar keys
       // collide on a few bins, and same-address smem atomics would serialise
-      const int64_t sg = ok ? seg_of(sd, head, t) - seg0 : 0;
+      const int64_t sg = !ok ? 0 : !tiny_win ? (int64_t)(t >= b1) : (int64_t)((uint32_t)(t - w0 * sd.win) / win32);
       const uint32_t dg = (__float_as_uint(s) >> (8 * (lane16 & 3))) & 255u;
       const bool act = ok && lane16 < 4;
       const unsigned amask = __ballot_sync(0xffffffffu, act);

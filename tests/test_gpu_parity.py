@@ -253,6 +253,70 @@ print("OK", ba.attention_kernel_name(q, k, v, B))
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("B", [128, 64])
+def test_running_max_grows_every_tile(ba, B):
+    """B = 128 pair kernel / B = 64 dual-tile kernel: key scale grows along the sequence, so in
+    ba_dense_attn (no permutation, key blocks walked in ascending order) the row max
+    of every tile exceeds the running max by far more than the lazy-rescale threshold
+    (2^8): every tile takes the rescale path, and with the speculative row max the
+    first P part is recomputed on every tile.  LSE checks the running max / sum."""
+    torch.manual_seed(11)
+    L, d, hq = 128 * 12 + 41, 128, 2
+    q = torch.randn(1, hq, L, d)
+    q[:, 1] *= -1.0  # the second head sees shrinking maxima along the walk (no rescale)
+    # key scale grows linearly: a row's tile max grows by ~7 nats (~10 log2 units) per key block
+    growth = 2.0 + 2.5 * torch.arange(L, dtype=torch.float32) / 128
+    k = (torch.randn(1, 1, L, d).abs() + 0.5) * growth[None, None, :, None]
+    v = torch.randn(1, 1, L, d)
+    q, k, v = (t.to(torch.bfloat16).cuda() for t in (q, k, v))
+    lse = torch.empty(1, hq, L, dtype=torch.float32, device="cuda")
+    out = ba.ba_dense_attn(q, k, v, lse=lse, block_size=B)
+    torch.cuda.synchronize()
+    scale = 1.0 / math.sqrt(d)
+    for h in range(hq):
+        qh, kh, vh = (t.double().cpu().numpy() for t in (q[0, h], k[0, 0], v[0, 0]))
+        ref = O.dense_attention(qh, kh, vh)
+        assert max_abs_err(out[0, h], ref) <= 2e-2, h
+        s = qh @ kh.T * scale
+        mx = s.max(axis=1)
+        ref_lse = mx + np.log(np.exp(s - mx[:, None]).sum(axis=1))
+        err = np.abs(lse[0, h].cpu().numpy() - ref_lse) / np.maximum(1.0, np.abs(ref_lse))
+        assert err.max() <= 1e-3, (h, float(err.max()))
+
+
+def test_pp_unequal_lists_split_steps(ba):
+    """Injected lists of unequal lengths (kv_count) with disjoint halves: the pair
+    kernel's walk runs shared tiles, split tiles (A and B on different key blocks) and
+    a one-sided tail (P = 0 for the block that ran out), with the ragged last key
+    block landing on each kind of step."""
+    w = CONFIGS["A"]
+    for seed in range(3):
+        q, k, v = make_qkv(w, device="cuda", seq_len=128 * 14 + 29, heads_q=2, heads_kv=1)
+        ctx = ba.Context(q, k, v, 128, 0.5)
+        sel = ctx.select(q, k, v)
+        nk, kap, nq = sel.n_k, sel.kappa, sel.n_q
+        rng = np.random.default_rng(100 + seed)
+        idx = np.zeros((2, nq, kap), np.int32)
+        cnt = np.zeros((2, nq), np.int32)
+        for h in range(2):
+            for g in range(nq):
+                c = int(rng.integers(1, kap + 1))
+                pick = np.sort(rng.choice(nk, c, replace=False))
+                if g % 3 == 0 and (nk - 1) not in pick:
+                    pick[-1] = nk - 1  # the ragged block on a split or one-sided step
+                    pick = np.unique(pick)
+                idx[h, g, :len(pick)] = pick
+                idx[h, g, len(pick):] = pick[-1]
+                cnt[h, g] = len(pick)
+        sel.kv_index.copy_(torch.from_numpy(idx[None]))
+        sel.kv_count.copy_(torch.from_numpy(cnt[None]))
+        out = torch.empty_like(q)
+        ctx.sparse_attn(out)
+        torch.cuda.synchronize()
+        err = max_abs_err(out, oracle_output_with_gpu_selection(q, k, v, sel, 128))
+        assert err <= 2e-2, (seed, err)
+
+
 @pytest.mark.parametrize("cfg,L,hq,hkv,b", [("A", 1024, 2, 2, 1), ("C", 2048 + 64, 8, 2, 2), ("A", 1000, 16, 16, 1)])
 def test_end_to_end_host_api(ba, cfg, L, hq, hkv, b):
     """ba_attention_host (chunked over KV heads, copies overlapped with compute)
