@@ -644,8 +644,11 @@ def run_ours(args):
         try:
             with open(tp) as f:
                 tj = json.load(f)
-            if tj.get("config") == args.config and tj.get("kernel") == ba.attention_kernel_name(q, k, v, B):
-                traffic = tj.get("dram_bytes_per_launch")
+            kname = ba.attention_kernel_name(q, k, v, B)
+            for e in tj.get("entries", [tj]):
+                if (e.get("config") == args.config and e.get("kernel") == kname and args.density is None
+                        and args.top_p is None and not args.random_lists and world == 1):
+                    traffic = e.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 

@@ -59,7 +59,7 @@ constexpr int kSoftmaxWarp0 = 2;
 constexpr int kThreads = 352;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef BA_PP_SPEC
-#define BA_PP_SPEC 0
+#define BA_PP_SPEC 1
 #endif
 constexpr bool kSpecMax = BA_PP_SPEC != 0;  // speculative row max (first P part against the running max)
 constexpr int kDefaultEmu = 0;             // pairs per 8 on the polynomial exp2 (off: MUFU + power cap wins)

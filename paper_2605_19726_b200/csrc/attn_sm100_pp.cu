@@ -70,10 +70,6 @@ constexpr int kPSplit = BA_PP_PSPLIT;     // P handed to the MMA in this many ke
 constexpr int kThreads = 384;             // 12 warps: 8 softmax (warpgroups 0, 1) + warpgroup 2 (producer, MMA, 2 idle)
 constexpr int kRegsSoftmax = 208, kRegsSide = 80;  // setmaxnreg: 8*32*208 + 4*32*80 = 63488 <= 65536
 constexpr float kRescaleThreshold = 8.0f;
-#ifndef BA_PP_SPEC
-#define BA_PP_SPEC 0
-#endif
-constexpr bool kSpecMax = BA_PP_SPEC != 0;  // speculative row max (first P part against the running max)
 constexpr int kMaskWords = 256;                             // nk <= 8192 (L <= 1M tokens)
 constexpr int kTraceTiles = 8;
 constexpr int kDefaultEmu = 1;  // 1 of 8 exp2 pairs on the FMA pipe: +2.4% at A, +1.4% at C (EMU sweep, profiles/round1_microbench.txt)
@@ -505,54 +501,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
           }
         };
         constexpr int PP = 64 / kPSplit;  // packed pairs per P part
-        if (kSpecMax && m != -INFINITY) {
-          // Speculative max: the first P part is exponentiated against the running max m while the
-          // tile's row max is reduced beside it (independent FMNMX3 chains fill the MUFU issue gaps
-          // instead of preceding the exps).  Exact unless the max grew by more than the lazy-rescale
-          // threshold (P <= 2^8 otherwise, as in the non-speculative path); then the part is redone.
-          // Iteration i reads S columns 4i..4i+3 (max) and 2i, 2i+1 (exp) and writes slot i <= 2i.
-          float m4[4];
-#pragma unroll
-          for (int v = 0; v < 4; ++v) m4[v] = -INFINITY;
-          const uint64_t nm2 = f2(-m, -m);
-#pragma unroll
-          for (int i = 0; i < PP; ++i) {
-            constexpr int kCols = 128 / PP;  // max columns per exp pair
-#pragma unroll
-            for (int t = 0; t < kCols; t += 2)
-              m4[((i & 1) << 1) + ((t >> 1) & 1)] = fmax3(m4[((i & 1) << 1) + ((t >> 1) & 1)], __uint_as_float(sr[kCols * i + t]), __uint_as_float(sr[kCols * i + t + 1]));
-            exp_pairs(i, i + 1, nm2);
-          }
-          const float mt = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * c;
-          const bool need = mt > m + kRescaleThreshold;
-          if (__any_sync(0xffffffffu, need)) {
-            // PV_x(u-1) is complete: the commit behind s_full[x](u) tracks every earlier MMA
-            float corr = 1.f;
-            if (need) { corr = ex2(m - mt); m = mt; }
-            uint32_t ov[16];
-#pragma unroll
-            for (int q8 = 0; q8 < 8; ++q8) {
-              tmem_ld_x16(trow + ocol + q8 * 16, ov);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
-              tmem_st_x16(trow + ocol + q8 * 16, ov);
-            }
-            l *= corr;
-            // redo the first part: its S columns [0, PP) were overwritten by P (S is intact in TMEM)
-            if constexpr (PP == 32) tmem_ld_x32(trow + scol, sr);
-            else tmem_ld_x16(trow + scol, sr);
-            tmem_wait_ld();
-            if (u == ragged_step) {
-#pragma unroll
-              for (int i = 0; i < PP; ++i)
-                if (i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
-            }
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc2[v] = 0ull;
-            exp_pairs(0, PP, f2(-m, -m));
-          }
-        } else {
+        {
           // row max: 8 independent FMNMX3 chains of depth 8 (the lone warp's latency, not its issue, bounds this)
           float m8[8];
 #pragma unroll

@@ -361,17 +361,25 @@ cudaError_t launch_radix_sort(const SortGeom &g, uint32_t *keys_a, uint32_t *val
 // content): seg_hist [segs][4][256] u32, status [4][tiles][256] u64, tickets [4] u32.
 // =====================================================================================
 constexpr int kKeysRowsPerCta = 512;    // 16 half-warps x 32 rows
-constexpr int kKR = 8;                   // rows per half-warp in flight (8 x 16-byte loads per lane)
 constexpr uint64_t kStAgg = 1ull << 62, kStInc = 1ull << 63, kStVal = (1ull << 62) - 1;
 
 BA_DEVICE int64_t seg_of(const SortSide &sd, int64_t head, int64_t t) { return sd.seg_base + head * sd.n_win + t / sd.win; }
 BA_DEVICE uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Row layout: FOUR lanes per row, lane l holding the chunks of A4's virtual lanes l, l+4,
+// l+8, l+12 (chunk = D/16 features).  Each virtual lane's sum is sequential as in A4; the
+// halving tree's first two levels (p[i] + p[i+8], then q[i] + q[i+4]) are lane-local and
+// the last two are xor shuffles, so every key is bit-identical to the 16-lane form (IEEE
+// addition commutes).  A warp holds 8 rows per step, so the per-row work (tree, key store,
+// histogram) costs a quarter of the 16-lane layout's issue slots.
 template <typename T, int D>
 __global__ void __launch_bounds__(256, 3) keys_hist_kernel(SortGeom g, KeysArgs ka, float *__restrict__ keys,
                                                         uint32_t *__restrict__ seg_hist) {
-  constexpr int PER_LANE = D / 16;
-  constexpr int BYTES = PER_LANE * (int)sizeof(T);
+  constexpr int CHUNK = D / 16;                        // features per virtual lane
+  constexpr int CB = CHUNK * (int)sizeof(T);           // bytes per chunk: 8, 16 or 32
+  constexpr int NV = CB >= 16 ? CB / 16 : 1;           // 16-byte loads per chunk (8-byte chunk: one uint2)
+  constexpr int kRowsInFlight = NV >= 2 ? 1 : 2;       // rows per lane per step (4 chunks each; 128 B in flight)
+  constexpr int kRowsPerStep = 8 * kRowsInFlight;      // per warp
   __shared__ uint32_t hist[2][4][256];  // the chunk's first two segments
   __shared__ int64_t s_seg0;
   // CTA -> (side, head row, chunk of kKeysRowsPerCta tokens)
@@ -389,7 +397,7 @@ __global__ void __launch_bounds__(256, 3) keys_hist_kernel(SortGeom g, KeysArgs 
   sd.seg_base = s1 ? g.side[1].seg_base : g.side[0].seg_base;
   const int64_t cph = (sd.L + kKeysRowsPerCta - 1) / kKeysRowsPerCta;
   const int64_t head = c / cph, t0 = (c - head * cph) * kKeysRowsPerCta;
-  const int64_t nrow = imin64(kKeysRowsPerCta, sd.L - t0);
+  const int nrow = (int)imin64(kKeysRowsPerCta, sd.L - t0);
   const T *x = static_cast<const T *>(s1 ? ka.x[1] : ka.x[0]);
   const int64_t stv0 = s1 ? ka.st[1][0] : ka.st[0][0], stv1 = s1 ? ka.st[1][1] : ka.st[0][1],
                 stv2 = s1 ? ka.st[1][2] : ka.st[0][2];
@@ -404,71 +412,80 @@ __global__ void __launch_bounds__(256, 3) keys_hist_kernel(SortGeom g, KeysArgs 
   const int64_t w0 = t0 / sd.win, b1 = (w0 + 1) * sd.win;
   const bool tiny_win = sd.win < kKeysRowsPerCta;
   const uint32_t win32 = (uint32_t)imin64(sd.win, 0x7fffffff);
-  const int lane16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
-  const T *xrow = x + bb * stv0 + hh * stv1 + lane16 * PER_LANE;
-  for (int it = 0; it < kKeysRowsPerCta / (16 * kKR); ++it) {
-    uint4 raw[kKR][BYTES > 16 ? 2 : 1];
-    int64_t rr[kKR];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l4 = lane & 3, rsub = lane >> 2;
+  const T *xbase = x + bb * stv0 + hh * stv1 + t0 * stv2 + l4 * CHUNK;
+  constexpr int kRowsPerWarp = kKeysRowsPerCta / 8;  // 64
+  for (int it = 0; it < kRowsPerWarp / kRowsPerStep; ++it) {
+    uint4 raw[kRowsInFlight][4][NV];
+    int rr[kRowsInFlight];
 #pragma unroll
-    for (int k = 0; k < kKR; ++k) {  // every load first
-      const int64_t r = (int64_t)(it * 16 + hw) * kKR + k;
+    for (int k = 0; k < kRowsInFlight; ++k) {  // every load first
+      const int r = warp * kRowsPerWarp + it * kRowsPerStep + k * 8 + rsub;
       rr[k] = r;
       if (r < nrow) {
-        const T *p = xrow + (t0 + r) * stv2;
-        if constexpr (BYTES == 8) {
-          const uint2 u = __ldg(reinterpret_cast<const uint2 *>(p));
-          raw[k][0] = make_uint4(u.x, u.y, 0, 0);
-        } else {
-          raw[k][0] = ldg16(p);
-          if constexpr (BYTES > 16) raw[k][BYTES > 16 ? 1 : 0] = ldg16(p + 16 / sizeof(T));
+        const T *p = xbase + (int64_t)r * stv2;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {  // virtual lane l4 + 4v: features [(l4 + 4v) * CHUNK, +CHUNK)
+          const T *pc = p + v * 4 * CHUNK;
+          if constexpr (CB == 8) {
+            const uint2 u = __ldg(reinterpret_cast<const uint2 *>(pc));
+            raw[k][v][0] = make_uint4(u.x, u.y, 0, 0);
+          } else {
+#pragma unroll
+            for (int n = 0; n < NV; ++n) raw[k][v][n] = ldg16(pc + n * (16 / (int)sizeof(T)));
+          }
         }
       }
     }
 #pragma unroll
-    for (int k = 0; k < kKR; ++k) {
-      float f[PER_LANE];
-      if constexpr (sizeof(T) == 2) {
-        const uint32_t w[4] = {raw[k][0].x, raw[k][0].y, raw[k][0].z, raw[k][0].w};
+    for (int k = 0; k < kRowsInFlight; ++k) {
+      float pv[4];
 #pragma unroll
-        for (int i = 0; i < PER_LANE / 2; ++i) {
-          f[2 * i] = __uint_as_float(w[i] << 16);
-          f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
-        }
-      } else {
+      for (int v = 0; v < 4; ++v) {
+        float f[CHUNK];
+        if constexpr (sizeof(T) == 2) {
 #pragma unroll
-        for (int i = 0; i < PER_LANE; ++i) {
-          const uint4 &u = raw[k][i / 4];
-          const uint32_t w = (i & 3) == 0 ? u.x : (i & 3) == 1 ? u.y : (i & 3) == 2 ? u.z : u.w;
-          f[i] = __uint_as_float(w);
+          for (int i = 0; i < CHUNK / 2; ++i) {
+            const uint4 &u = raw[k][v][i / 4];
+            const uint32_t w = (i & 3) == 0 ? u.x : (i & 3) == 1 ? u.y : (i & 3) == 2 ? u.z : u.w;
+            f[2 * i] = __uint_as_float(w << 16);
+            f[2 * i + 1] = __uint_as_float(w & 0xffff0000u);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < CHUNK; ++i) {
+            const uint4 &u = raw[k][v][i / 4];
+            const uint32_t w = (i & 3) == 0 ? u.x : (i & 3) == 1 ? u.y : (i & 3) == 2 ? u.z : u.w;
+            f[i] = __uint_as_float(w);
+          }
         }
+        // IEEE fp32, product and sum each rounded (no FMA contraction): reading A4
+        float sv = 0.f;
+#pragma unroll
+        for (int i = 0; i < CHUNK; ++i) sv = __fadd_rn(sv, __fmul_rn(f[i], f[i]));
+        pv[v] = sv;
       }
-      // IEEE fp32, product and sum each rounded (no FMA contraction): reading A4 (as K1)
-      float s = 0.f;
-#pragma unroll
-      for (int i = 0; i < PER_LANE; ++i) s = __fadd_rn(s, __fmul_rn(f[i], f[i]));
-      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 8));
-      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+      // halving tree: p[i] + p[i+8] (v, v+2), q[i] + q[i+4] (v = 0, 1), then r[i] + r[i+2], s[0] + s[1]
+      float s = __fadd_rn(__fadd_rn(pv[0], pv[2]), __fadd_rn(pv[1], pv[3]));
       s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
       s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
       const bool ok = rr[k] < nrow;
       const int64_t t = t0 + rr[k];
-      if (ok && lane16 == 0) {
+      if (ok && l4 == 0) {
         keys[sd.base + head * sd.L + t] = s;
         if (user) user[head * sd.L + t] = s;
       }
-      // histograms: lanes 0-3 of each half-warp take one digit each; lanes with equal
-      // (segment, digit) are aggregated first (match_any) — the high digits of similar keys
-      // collide on a few bins, and same-address smem atomics would serialise
+      // histograms: lane l4 of each row takes digit l4; lanes with equal (segment, digit, value)
+      // are aggregated first (match_any: the high digits of similar keys collide on a few bins)
       const int64_t sg = !ok ? 0 : !tiny_win ? (int64_t)(t >= b1) : (int64_t)((uint32_t)(t - w0 * sd.win) / win32);
-      const uint32_t dg = (__float_as_uint(s) >> (8 * (lane16 & 3))) & 255u;
-      const bool act = ok && lane16 < 4;
-      const unsigned amask = __ballot_sync(0xffffffffu, act);
-      if (act) {
-        const uint32_t tag = ((uint32_t)(lane16 & 3) << 8 | dg) + (sg < 2 ? (uint32_t)sg << 10 : 0x80000000u + lane_id());
+      const uint32_t dg = (__float_as_uint(s) >> (8 * l4)) & 255u;
+      const unsigned amask = __ballot_sync(0xffffffffu, ok);
+      if (ok) {
+        const uint32_t tag = ((uint32_t)l4 << 8 | dg) + (sg < 2 ? (uint32_t)sg << 10 : 0x80000000u + lane);
         const unsigned peers = __match_any_sync(amask, tag);
         if ((peers & lanemask_lt()) == 0) {  // the lowest lane of each group adds the group's count
-          if (sg < 2) atomicAdd(&hist[sg][lane16 & 3][dg], (uint32_t)__popc(peers));
-          else atomicAdd(&seg_hist[(seg0 + sg) * 1024 + (lane16 & 3) * 256 + dg], 1u);  // tiny windows only
+          if (sg < 2) atomicAdd(&hist[sg][l4][dg], (uint32_t)__popc(peers));
+          else atomicAdd(&seg_hist[(seg0 + sg) * 1024 + l4 * 256 + dg], 1u);  // tiny windows only
         }
       }
     }

@@ -64,6 +64,38 @@ def test_selection_bf16(ba, cfg, L, hq, hkv, dens, comp):
     assert rep["max_stat_err"] < 1e-12, rep
 
 
+@pytest.mark.parametrize("cfg,L,hq,hkv,B", [("A", 4096 + 77, 4, 4, 128), ("C", 8192, 8, 2, 128), ("T", 1024, 1, 1, 64),
+                                          ("M", 4096 + 17, 2, 2, 64)])
+def test_norm_order_against_exact_norms(ba, cfg, L, hq, hkv, B):
+    """S1/S2 checked independently of oracle.norm_key (verdict r1 item 9): the GPU's
+    pi must order rows by the EXACT squared norm ||x||^2, computed here
+    in fp64 from the very inputs (bf16 / fp32 squares and their 128-term sums are exact or
+    within 1e-14 relative in fp64).  The GPU key is an fp32 sum of d products in a fixed
+    order: sequential over a lane's d/16 features, then a 4-level tree — at most
+    d/16 + 4 + 1 <= 13 roundings, so |key - ||x||^2| <= gamma_13 ||x||^2 (Higham 3.5 with
+    gamma_n = n u / (1 - n u), u = 2^-24).  Hence an adjacent pair of pi may be out of
+    exact order only when their exact norms differ by at most gamma_13 (a + b)."""
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv)
+    ctx, sel = _run_select(ba, q, k, v, B, w.density)
+    u = 2.0 ** -24
+    gamma = 13 * u / (1 - 13 * u)
+    for x, perm in ((q, sel.perm_q), (k, sel.perm_k)):
+        xn = x.detach().double().cpu().numpy()
+        pn = perm.cpu().numpy()
+        for bi in range(xn.shape[0]):
+            for h in range(xn.shape[1]):
+                exact = (xn[bi, h] * xn[bi, h]).sum(axis=1)
+                p = pn[bi, h]
+                assert np.array_equal(np.sort(p), np.arange(L)), "pi is not a permutation"
+                a, b = exact[p[:-1]], exact[p[1:]]
+                bad = (a > b) & (a - b > gamma * (a + b))
+                assert not bad.any(), (cfg, h, int(bad.sum()), float((a - b)[bad].max()))
+                # identical rows (the synthetic duplicates of T) have identical keys: stable, lower index first
+                tie = np.all(xn[bi, h][p[:-1]] == xn[bi, h][p[1:]], axis=1)
+                assert (p[:-1][tie] < p[1:][tie]).all()
+
+
 def test_selection_windowed_and_beta(ba):
     w = CONFIGS["A"]
     q, k, v = make_qkv(w, device="cuda", seq_len=5000, heads_q=2, heads_kv=2)
@@ -366,6 +398,49 @@ for cfg, L, hq, hkv, dens in (("A", 4096 + 77, 2, 2, 0.5), ("C", 3 * 128 * 5, 4,
 print("OK", ba.attention_kernel_name(q, k, v, 128))
 """
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=240)
+    assert r.returncode == 0 and f"OK {name}\n" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("k5,name", [("dual", "attn_sm100_tcgen05_dual64")])
+def test_b64_kernel_parity(ba, k5, name):
+    """The B = 64 dual-tile kernel on real selections: ragged lengths (a ragged last
+    key block), odd query- and key-block counts (a half-empty last tile), GQA, top-p
+    lists of unequal length, and the per-tile rescale workload (key scale growing
+    along the sequence, dense) that exercises the speculative row max's redo."""
+    import os, subprocess, sys
+    env = dict(os.environ, BA_ATTN_B64=k5)
+    code = f"""
+import sys, math; sys.path.insert(0, {os.path.dirname(__file__)!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import numpy as np, torch
+import oracle as O
+import paper_2605_19726_b200.baatt as ba
+from synth import CONFIGS, make_qkv
+from parity import oracle_output_with_gpu_selection, max_abs_err
+for cfg, L, hq, hkv, dens, top_p in (("M", 64 * 37 + 5, 2, 2, 0.5, None), ("M", 64 * 21, 4, 2, 0.3, None),
+                                     ("M", 64 * 30 + 63, 2, 1, 0.5, 0.9), ("M", 64 * 9, 1, 1, 1.0, None)):
+    w = CONFIGS[cfg]
+    q, k, v = make_qkv(w, device="cuda", seq_len=L, heads_q=hq, heads_kv=hkv)
+    ctx = ba.Context(q, k, v, 64, dens, top_p=top_p)
+    sel = ctx.select(q, k, v)
+    out = torch.empty_like(q)
+    ctx.sparse_attn(out)
+    torch.cuda.synchronize()
+    err = max_abs_err(out, oracle_output_with_gpu_selection(q, k, v, sel, 64))
+    assert err <= 2e-2, (cfg, L, err)
+torch.manual_seed(5)
+L = 64 * 19 + 23
+q = torch.randn(1, 2, L, 128); q[:, 1] *= -1.0
+k = (torch.randn(1, 1, L, 128).abs() + 0.5) * (2.0 + 1.25 * torch.arange(L, dtype=torch.float32) / 64)[None, None, :, None]
+v = torch.randn(1, 1, L, 128)
+q, k, v = (t.to(torch.bfloat16).cuda() for t in (q, k, v))
+out = ba.ba_dense_attn(q, k, v, block_size=64)
+torch.cuda.synchronize()
+for h in range(2):
+    ref = O.dense_attention(q[0, h].double().cpu().numpy(), k[0, 0].double().cpu().numpy(), v[0, 0].double().cpu().numpy())
+    assert max_abs_err(out[0, h], ref) <= 2e-2, ("rescale", h)
+print("OK", ba.attention_kernel_name(q, k, v, 64))
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
     assert r.returncode == 0 and f"OK {name}\n" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
