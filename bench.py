@@ -256,7 +256,7 @@ def run_reference(args):
         tot_s += secs
     value = tot_fl / tot_s / 1e12
     cores = cpu_cores()
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+    line = {"impl": "reference", "schema": "ba-bench-line/2", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak" if args.shard == "batch" else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -667,7 +667,7 @@ def run_ours(args):
             par = f"batch-parallel x{world} (weak scaling, no data-path collective)"
         kernel = ba.attention_kernel_name(q, k, v, B) if not dry else "dry-run stand-in"
         line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "schema": "ba-bench-line/2", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if heads else "weak",
             "vs_baseline": None, "dtype": "bf16" if w.dtype == "bf16" else "fp32", "data": "synthetic",

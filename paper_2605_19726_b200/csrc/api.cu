@@ -1,5 +1,6 @@
 // api.cu — the C ABI of libbaatt.so (include/ba_attn.h): validation,
 // workspace carving and the launch sequence of Alg. 1.
+#include <nvtx3/nvToolsExt.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -182,6 +183,16 @@ SelBufPlan plan_selbufs(const Dims &D, bool no_q = false, bool kv = true) {
   return p;
 }
 
+// NVTX ranges around every stage the library enqueues (header-only NVTX v3: a no-op
+// unless a tool is attached), so ncu --nvtx --nvtx-include "ba_select/..." can pick
+// the kernels of one stage.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 template <typename P>
 P *at(void *ws, size_t off) { return reinterpret_cast<P *>(static_cast<char *>(ws) + off); }
 
@@ -210,6 +221,7 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   if (plan.total && !ws) return fail(BA_ERR_INVALID_ARGUMENT, "workspace is NULL");
   if (reinterpret_cast<uintptr_t>(ws) % kAlign) return fail(BA_ERR_SHAPE_MISMATCH, "workspace is not 256-byte aligned");
 
+  NvtxRange nv_select("ba_select");
   int launches = 0;
   SortGeom g = make_geom(D, pa);
   g.side[0].perm_out = nullptr;
@@ -218,6 +230,7 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   // K1 + K2: norm keys of the sorted sides with their digit histograms, then the four onesweep
   // passes -> perm_q / perm_k (1 memset + 5 launches); keys of an unsorted side only when asked for
   {
+    NvtxRange nv("ba_select/K1+K2 norm keys, histograms, onesweep sort");
     KeysArgs ka{};
     ka.batch = D.b;
     int si = 0;
@@ -247,6 +260,7 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   double *k_mean = sel->k_mean ? sel->k_mean : at<double>(ws, plan.k_mean);
   double *k_var = sel->k_var ? sel->k_var : at<double>(ws, plan.k_var);
   {  // Q, K (+ V copy) in one launch
+    NvtxRange nv("ba_select/K3 permute + block moments");
     GatherSides gs;
     auto side = [&](const void *x, const int64_t *stv, int64_t heads, int64_t L, const int32_t *perm,
                     int32_t *perm_id_out, void *xs, double *mean, double *var) {
@@ -279,6 +293,7 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
     launches += 2;
     qv = q_cov; kv = k_cov; comp = 2;
   }
+  NvtxRange nv_k4("ba_select/K4 compensated scores + top-kappa");
   BA_TRY(cuda_check(launch_scores_topk((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, qv, k_mean, kv, comp,
                                        (double)pa->beta, logits, D.kappa, top_p, sel->kv_index, sel->kv_count,
                                        sel->mask, sel->block_prob, sel->threshold, st), "scores_topk"));
@@ -395,6 +410,7 @@ ba_status take_device_errors() {
 
 ba_status run_attn(AttnArgs a, cudaStream_t st) {
   if (const char *why = attn_unsupported(a)) return fail(BA_ERR_UNSUPPORTED, "%s", why);
+  NvtxRange nv("ba_sparse_attn");
   a.err_flag = err_flag_dev();
   cudaError_t e;
   if (use_pp2(a)) e = launch_attn_pp2(a, st);

@@ -70,6 +70,16 @@ constexpr int kPSplit = BA_PP_PSPLIT;     // P handed to the MMA in this many ke
 constexpr int kThreads = 384;             // 12 warps: 8 softmax (warpgroups 0, 1) + warpgroup 2 (producer, MMA, 2 idle)
 constexpr int kRegsSoftmax = 208, kRegsSide = 80;  // setmaxnreg: 8*32*208 + 4*32*80 = 63488 <= 65536
 constexpr float kRescaleThreshold = 8.0f;
+#ifndef BA_PP_EMU0
+#define BA_PP_EMU0 -1
+#endif
+#ifndef BA_PP_EMU1
+#define BA_PP_EMU1 -1
+#endif
+#ifndef BA_PP_DEFER_SUM
+#define BA_PP_DEFER_SUM 1
+#endif
+constexpr bool kDeferSum = BA_PP_DEFER_SUM != 0;
 constexpr int kMaskWords = 256;                             // nk <= 8192 (L <= 1M tokens)
 constexpr int kTraceTiles = 8;
 constexpr int kDefaultEmu = 1;  // 1 of 8 exp2 pairs on the FMA pipe: +2.4% at A, +1.4% at C (EMU sweep, profiles/round1_microbench.txt)
@@ -173,6 +183,8 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kSlots = NSLOT;
+  // exp2 offload per P part (A/B knobs BA_PP_EMU0 / BA_PP_EMU1; default kEmu for both)
+  constexpr int kEmu0 = BA_PP_EMU0 >= 0 ? BA_PP_EMU0 : kEmu, kEmu1 = BA_PP_EMU1 >= 0 ? BA_PP_EMU1 : kEmu;
   constexpr bool kTrace = kMode == 2;
   long long(*trace)[kTraceTiles] = reinterpret_cast<long long(*)[kTraceTiles]>(smem + SMEM_TRACE);
   const bool tr = kTrace && blockIdx.x == 0 && blockIdx.y == 0;
@@ -448,12 +460,17 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     const float c = a.scale * 1.4426950408889634f;
     float m = -INFINITY, l = 0.f;
     uint32_t sr[128];
+    // kDeferSum: the exps overwrite S in sr (fp32) and the packed P goes to pk; the row sum
+    // is reduced after the P parts are published (off the path to the PV MMA, as cuDNN's
+    // sm100 kernel does); otherwise P is packed over sr[0..63] and summed inline.
+    uint32_t pk[kDeferSum ? 64 : 1];
+    uint32_t *pp = kDeferSum ? pk : sr;
     // P (bf16 pairs) over S in TMEM: part q = keys 128q/kPSplit .. -> columns 64q/kPSplit ..
     // (S of those columns is already in registers), then p_part[q]
     auto publish_part = [&](int q) {
       constexpr int W = 64 / kPSplit;  // TMEM columns per part
-      if constexpr (W == 32) tmem_st_x32(trow + scol + W * q, sr + W * q);
-      else tmem_st_x16(trow + scol + W * q, sr + W * q);
+      if constexpr (W == 32) tmem_st_x32(trow + scol + W * q, pp + W * q);
+      else tmem_st_x16(trow + scol + W * q, pp + W * q);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -467,7 +484,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       tc_fence_after();
       if (kMode == 1) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) sr[i] = 0u;
+        for (int i = 0; i < 64; ++i) pp[i] = 0u;
         if (mine) l = 1.f, m = 0.f;
       } else if (mine) {
 #pragma unroll
@@ -487,17 +504,22 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
           for (int i = i0; i < i1; ++i) {
             const uint64_t x2 = ffma2(f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), c2, nm2);
             uint64_t p2;
-            if ((i & 7) < kEmu) {
+            if ((i & 7) < (i < 32 ? kEmu0 : kEmu1)) {
               p2 = exp2_poly2(x2);
             } else {
               float x0, x1;
               unf2(x2, x0, x1);
               p2 = f2(ex2(x0), ex2(x1));
             }
-            acc2[i & 3] = fadd2(acc2[i & 3], p2);
             float p0, p1;
             unf2(p2, p0, p1);
-            sr[i] = pack_bf16(p0, p1);
+            if constexpr (kDeferSum) {
+              sr[2 * i] = __float_as_uint(p0);
+              sr[2 * i + 1] = __float_as_uint(p1);
+            } else {
+              acc2[i & 3] = fadd2(acc2[i & 3], p2);
+            }
+            pp[i] = pack_bf16(p0, p1);
           }
         };
         constexpr int PP = 64 / kPSplit;  // packed pairs per P part
@@ -540,6 +562,12 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
           exp_pairs(PP * h2, PP * h2 + PP, nm2);
           if (h2 < kPSplit - 1) publish_part(h2);
         }
+        if constexpr (kDeferSum) {
+          publish_part(kPSplit - 1);
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            acc2[i & 3] = fadd2(acc2[i & 3], f2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])));
+        }
         const uint64_t t2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
         float a0, a1;
         unf2(t2, a0, a1);
@@ -547,7 +575,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
         if (trx) TR(6 + 4 * x, u);
       } else {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) sr[i] = 0u;  // block not selected by these rows: P = 0
+        for (int i = 0; i < 64; ++i) pp[i] = 0u;  // block not selected by these rows: P = 0
 #pragma unroll
         for (int q = 0; q < kPSplit - 1; ++q) publish_part(q);
       }
@@ -555,7 +583,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
 #pragma unroll
         for (int q = 0; q < kPSplit - 1; ++q) publish_part(q);
       }
-      publish_part(kPSplit - 1);
+      if (!kDeferSum || kMode == 1 || !mine) publish_part(kPSplit - 1);
       if (trx) TR(7 + 4 * x, u);
     }
     if (cnt > 0) {
