@@ -1170,6 +1170,120 @@ BA_DEVICE void scores_tile(int64_t hq, int64_t grp, int64_t nq, int64_t nk, cons
   }
 }
 
+// The diagonal-compensation tile with fewer, larger warp tiles (K4a, default): 8 warps of
+// 32 x 64 outputs (4 x 8 DMMA tiles, 64 fp64 accumulators per thread), 16 features per smem
+// stage (4 k-steps, half the CTA barriers of the 32 x 32 / 8-feature form), the next
+// k-step's fragments loaded while the current k-step's 32 DMMAs issue, and per stage only
+// the operand arrays that stage's feature part needs (a stage never straddles a part).
+// Measured (ncu, config A) the 32 x 32 form stalled on smem fragment latency (short
+// scoreboard 19%) and barriers (14%) as much as on the FP64 pipe (20%).
+constexpr int kScW_KS = 16, kScW_LDS = 128 + 8;
+struct ScoresSmemW {
+  double A[2][kScW_KS][kScW_LDS];
+  double B[2][kScW_KS][kScW_LDS];
+};
+template <int D>
+BA_DEVICE void scores_tile_w(int64_t hq, int64_t grp, int64_t nq, int64_t nk, const double *__restrict__ q_mean,
+                             const double *__restrict__ q_var, const double *__restrict__ k_mean,
+                             const double *__restrict__ k_var, int comp, double inv_sqrt_d, double beta_over_d,
+                             double *__restrict__ logits, int64_t bhq, int64_t gq0, int64_t gk0, ScoresSmemW &sm) {
+  constexpr int TILE = 128, KS = kScW_KS, LPT = TILE * KS / 256;  // 8 features per thread per operand per stage
+  static_assert(D % KS == 0, "a stage never straddles a feature part");
+  const int64_t b = bhq / hq, h = bhq - b * hq;
+  const int64_t bhk = b * (hq / grp) + h / grp;
+  const double *qm = q_mean + bhq * nq * D, *qv = q_var + bhq * nq * D;
+  const double *km = k_mean + bhk * nk * D, *kv = k_var + bhk * nk * D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = (warp >> 1) * 32, wc = (warp & 1) * 64;  // warp tile origin
+  const int g = lane >> 2, tq = lane & 3;
+  double acc[4][8][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int nfeat = comp ? 3 * D : D;
+  const int lr = threadIdx.x >> 1, lf = (threadIdx.x & 1) * LPT;  // loader: row lr, features lf .. lf + 7
+  const bool q_ok = gq0 + lr < nq, k_ok = gk0 + lr < nk;
+  const double *qrow_m = qm + (gq0 + lr) * D + lf, *qrow_v = qv + (gq0 + lr) * D + lf;
+  const double *krow_m = km + (gk0 + lr) * D + lf, *krow_v = kv + (gk0 + lr) * D + lf;
+  double r0[LPT], r1[LPT], r2[LPT];  // part 0: qm, km; part 1: qv, km, kv; part 2: qm, kv
+  auto ld8 = [](double *dst, const double *src, bool ok) {
+#pragma unroll
+    for (int e = 0; e < LPT; e += 2) {
+      const double2 v = ok ? __ldg(reinterpret_cast<const double2 *>(src + e)) : make_double2(0.0, 0.0);
+      dst[e] = v.x;
+      dst[e + 1] = v.y;
+    }
+  };
+  auto fetch = [&](int c0) {
+    const int part = c0 / D, t = c0 - part * D;
+    if (part == 0) { ld8(r0, qrow_m + t, q_ok); ld8(r1, krow_m + t, k_ok); }
+    else if (part == 1) { ld8(r0, qrow_v + t, q_ok); ld8(r1, krow_m + t, k_ok); ld8(r2, krow_v + t, k_ok); }
+    else { ld8(r0, qrow_m + t, q_ok); ld8(r2, krow_v + t, k_ok); }
+  };
+  auto stash = [&](int c0, int buf) {  // Xq = [Qbar/sqrt(d), (beta/d) VarQ, (beta/d) Qbar^2], Xk = [Kbar, Kbar^2 + VarK, VarK]
+    const int part = c0 / D;
+#pragma unroll
+    for (int e = 0; e < LPT; ++e) {
+      double xa, xb;
+      if (part == 0) { xa = r0[e] * inv_sqrt_d; xb = r1[e]; }
+      else if (part == 1) { xa = beta_over_d * r0[e]; xb = fma(r1[e], r1[e], r2[e]); }
+      else { xa = beta_over_d * (r0[e] * r0[e]); xb = r2[e]; }
+      sm.A[buf][lf + e][lr] = xa;
+      sm.B[buf][lf + e][lr] = xb;
+    }
+  };
+  fetch(0);
+  stash(0, 0);
+  __syncthreads();
+  int buf = 0;
+  for (int c0 = 0; c0 < nfeat; c0 += KS) {
+    const bool more = c0 + KS < nfeat;
+    if (more) fetch(c0 + KS);  // global loads in flight during the DMMAs below
+    double af[2][4], bf[2][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) af[0][i] = sm.A[buf][tq][wr + 8 * i + g];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bf[0][j] = sm.B[buf][tq][wc + 8 * j + g];
+#pragma unroll
+    for (int s4 = 0; s4 < KS / 4; ++s4) {
+      const int cur = s4 & 1;
+      if (s4 + 1 < KS / 4) {  // next k-step's fragments ahead of this k-step's DMMAs
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[cur ^ 1][i] = sm.A[buf][4 * (s4 + 1) + tq][wr + 8 * i + g];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bf[cur ^ 1][j] = sm.B[buf][4 * (s4 + 1) + tq][wc + 8 * j + g];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                       : "d"(af[cur][i]), "d"(bf[cur][j]));
+    }
+    if (more) stash(c0 + KS, buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gq = gq0 + wr + 8 * i + g;
+    if (gq >= nq) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t gk = gk0 + wc + 8 * j + 2 * tq;
+      double *dst = logits + (bhq * nq + gq) * nk + gk;
+      if (gk + 1 < nk && ((nk & 1) == 0)) {
+        *reinterpret_cast<double2 *>(dst) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        if (gk < nk) dst[0] = acc[i][j][0];
+        if (gk + 1 < nk) dst[1] = acc[i][j][1];
+      }
+    }
+  }
+}
+
 template <int D, int TILE, int KS, bool kExact = false>
 __global__ void __launch_bounds__((TILE / 32) * (TILE / 32) * 32) scores_mma_kernel(
     int64_t hq, int64_t grp, int64_t nq, int64_t nk, const double *__restrict__ q_mean,
@@ -1434,8 +1548,8 @@ __global__ void topk_kernel(int64_t rows, int64_t nk, int64_t kappa, double top_
 // synchronises once, and then every warp selects rows (grid-strided) — the top-kappa needs
 // complete rows, hence the grid-wide barrier.  Shared memory: the score tiles' operand
 // stages, reused by the top-kappa rows afterwards.
-template <int D, bool kExact>
-__global__ void __launch_bounds__(512, 1) scores_topk_kernel(int64_t hq, int64_t grp, int64_t nq, int64_t nk,
+template <int D, bool kExact, bool kWide>
+__global__ void __launch_bounds__(kWide ? 256 : 512, 1) scores_topk_kernel(int64_t hq, int64_t grp, int64_t nq, int64_t nk,
                                                             const double *__restrict__ q_mean,
                                                             const double *__restrict__ q_var,
                                                             const double *__restrict__ k_mean,
@@ -1447,13 +1561,17 @@ __global__ void __launch_bounds__(512, 1) scores_topk_kernel(int64_t hq, int64_t
                                                             double *__restrict__ prob, double *__restrict__ tau,
                                                             int topk_warps) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto &sm = *reinterpret_cast<ScoresSmem<128, kScoresKS> *>(smem_raw);
   const int64_t tq = (nq + 127) / 128, tk = (nk + 127) / 128;
   const int64_t tiles = tq * tk * bh_total;
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     const int64_t bhq = t / (tq * tk), r = t - bhq * tq * tk, iq = r / tk, ik = r - iq * tk;
-    scores_tile<D, 128, kScoresKS, kExact>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, beta_over_d,
-                                           logits, bhq, iq * 128, ik * 128, sm);
+    if constexpr (kWide)
+      scores_tile_w<D>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, beta_over_d, logits, bhq,
+                       iq * 128, ik * 128, *reinterpret_cast<ScoresSmemW *>(smem_raw));
+    else
+      scores_tile<D, 128, kScoresKS, kExact>(hq, grp, nq, nk, q_mean, q_var, k_mean, k_var, comp, inv_sqrt_d, beta_over_d,
+                                             logits, bhq, iq * 128, ik * 128,
+                                             *reinterpret_cast<ScoresSmem<128, kScoresKS> *>(smem_raw));
     __syncthreads();  // the operand stages are reused by the next tile
   }
   __threadfence();
@@ -1474,17 +1592,24 @@ cudaError_t launch_scores_topk(int d, int64_t batch, int64_t hq, int64_t hkv, in
   const double inv_sqrt_d = 1.0 / sqrt((double)d), bod = beta / (double)d;
   int64_t grp = hq / hkv, bh_total = batch * hq;
   constexpr size_t kMaxSmem = 227 * 1024;
+  // the wide-tile DMMA form (8 warps) for the diagonal / no compensation; the exact
+  // covariance form keeps the 16-warp 32 x 32 tiles (BA_SCORES_NARROW=1: A/B knob)
+  static int narrow = -1;
+  if (narrow < 0) narrow = getenv("BA_SCORES_NARROW") ? atoi(getenv("BA_SCORES_NARROW")) : 0;
+  const bool wide = comp != 2 && !narrow;
+  const int threads = wide ? 256 : 512;
   const size_t per_warp = (size_t)nk * sizeof(double) + 256 * sizeof(unsigned);
-  int topk_warps = (int)std::min<size_t>(16, kMaxSmem / per_warp);
+  int topk_warps = (int)std::min<size_t>(threads / 32, kMaxSmem / per_warp);
   if (topk_warps < 1) return cudaErrorInvalidValue;  // N_k beyond the shared-memory row buffer (validated earlier)
-  size_t smem = std::max(sizeof(ScoresSmem<128, kScoresKS>), (size_t)topk_warps * per_warp);
+  size_t smem = std::max(wide ? sizeof(ScoresSmemW) : sizeof(ScoresSmem<128, kScoresKS>), (size_t)topk_warps * per_warp);
   void *kernel;
-  if (comp == 2) kernel = d == 128 ? (void *)scores_topk_kernel<128, true> : (void *)scores_topk_kernel<64, true>;
-  else kernel = d == 128 ? (void *)scores_topk_kernel<128, false> : (void *)scores_topk_kernel<64, false>;
+  if (comp == 2) kernel = d == 128 ? (void *)scores_topk_kernel<128, true, false> : (void *)scores_topk_kernel<64, true, false>;
+  else if (wide) kernel = d == 128 ? (void *)scores_topk_kernel<128, false, true> : (void *)scores_topk_kernel<64, false, true>;
+  else kernel = d == 128 ? (void *)scores_topk_kernel<128, false, false> : (void *)scores_topk_kernel<64, false, false>;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0, dev = 0, sms = 0;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 512, smem)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem)) != cudaSuccess) return e;
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorLaunchOutOfResources;
@@ -1497,7 +1622,7 @@ cudaError_t launch_scores_topk(int d, int64_t batch, int64_t hq, int64_t hkv, in
   void *args[] = {&hq, &grp, &nq, &nk, (void *)&q_mean, (void *)&q_var, (void *)&k_mean, (void *)&k_var, &comp,
                   (void *)&inv_sqrt_d, (void *)&bod, &logits, &bh_total, &kappa, &top_p, &kv_index, &kv_count, &mask,
                   &prob, &tau, &topk_warps};
-  return cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(512), args, smem, st);
+  return cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(threads), args, smem, st);
 }
 
 cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *logits,
