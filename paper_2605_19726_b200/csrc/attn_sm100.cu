@@ -63,7 +63,7 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #endif
 constexpr bool kSpecMax = BA_PP_SPEC != 0;  // speculative row max (first P part against the running max)
 constexpr int kDefaultEmu = 0;             // pairs per 8 on the polynomial exp2 (off: MUFU + power cap wins)
-constexpr int kDefaultEmu64 = 1;           // dual-tile (B = 64) kernel
+constexpr int kDefaultEmu64 = 0;           // dual-tile (B = 64) kernel: MUFU only (M: 1012-1020 TF/s vs 1002 at 1 of 8, 973 at 2 of 8; profiles/round2_b64_emu.json)
 constexpr int kMaskWords = 1024;           // bitmask capacity: N_k <= 32768 key blocks
 
 template <int kBN>
