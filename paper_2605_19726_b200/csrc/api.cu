@@ -296,8 +296,7 @@ ba_status run_select(const Dims &D, const ba_problem *prob, const ba_params *pa,
   NvtxRange nv_k4("ba_select/K4 compensated scores + top-kappa");
   BA_TRY(cuda_check(launch_scores_topk((int)D.d, D.b, D.hq, D.hkv, D.nq, D.nk, q_mean, qv, k_mean, kv, comp,
                                        (double)pa->beta, logits, D.kappa, top_p, sel->kv_index, sel->kv_count,
-                                       sel->mask, sel->block_prob, sel->threshold, st), "scores_topk"));
-  launches += 1;
+                                       sel->mask, sel->block_prob, sel->threshold, st, &launches), "scores_topk"));
   g_launches = launches;
   return BA_OK;
 }

@@ -99,7 +99,7 @@ constexpr int64_t kSelectMaxNk = 28672;
 cudaError_t launch_scores_topk(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk,
                                const double *q_mean, const double *q_var, const double *k_mean, const double *k_var,
                                int comp, double beta, double *logits, int64_t kappa, double top_p, int32_t *kv_index,
-                               int32_t *kv_count, uint8_t *mask, double *prob, double *tau, cudaStream_t st);
+                               int32_t *kv_count, uint8_t *mask, double *prob, double *tau, cudaStream_t st, int *launches);
 // top_p > 0: cumulative-mass budget (reading A23), kappa = the cap and the kv_index row stride
 cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *logits,
                         int32_t *kv_index, int32_t *kv_count, uint8_t *mask, double *prob,

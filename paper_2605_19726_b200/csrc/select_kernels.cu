@@ -1585,10 +1585,14 @@ __global__ void __launch_bounds__(kWide ? 256 : 512, 1) scores_topk_kernel(int64
     topk_row(row, nk, kappa, top_p, logits, kv_index, kv_count, mask, prob, tau, x, hist_base + warp * 256);
 }
 
+cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *logits,
+                        int32_t *kv_index, int32_t *kv_count, uint8_t *mask, double *prob, double *tau,
+                        cudaStream_t st);
+
 cudaError_t launch_scores_topk(int d, int64_t batch, int64_t hq, int64_t hkv, int64_t nq, int64_t nk,
                                const double *q_mean, const double *q_var, const double *k_mean, const double *k_var,
                                int comp, double beta, double *logits, int64_t kappa, double top_p, int32_t *kv_index,
-                               int32_t *kv_count, uint8_t *mask, double *prob, double *tau, cudaStream_t st) {
+                               int32_t *kv_count, uint8_t *mask, double *prob, double *tau, cudaStream_t st, int *launches) {
   const double inv_sqrt_d = 1.0 / sqrt((double)d), bod = beta / (double)d;
   int64_t grp = hq / hkv, bh_total = batch * hq;
   constexpr size_t kMaxSmem = 227 * 1024;
@@ -1619,10 +1623,20 @@ cudaError_t launch_scores_topk(int d, int64_t batch, int64_t hq, int64_t hkv, in
   const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)per_sm * sms);
   double kap_d = 0;
   (void)kap_d;
+  // The top-kappa rows run as their own launch by default: after the grid barrier the fused
+  // phase had one 8-warp CTA per SM and was latency-bound (C: selection 3.32 -> 3.02 ms, A
+  // 0.717 -> 0.699 ms split; profiles/round2_k4_split.json).  BA_K4_SPLIT=0: fused (A/B knob).
+  static int split = -1;
+  if (split < 0) split = getenv("BA_K4_SPLIT") ? atoi(getenv("BA_K4_SPLIT")) : 1;
+  int tw = split ? 0 : topk_warps;
   void *args[] = {&hq, &grp, &nq, &nk, (void *)&q_mean, (void *)&q_var, (void *)&k_mean, (void *)&k_var, &comp,
                   (void *)&inv_sqrt_d, (void *)&bod, &logits, &bh_total, &kappa, &top_p, &kv_index, &kv_count, &mask,
-                  &prob, &tau, &topk_warps};
-  return cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(threads), args, smem, st);
+                  &prob, &tau, &tw};
+  e = cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(threads), args, smem, st);
+  if (launches) ++*launches;
+  if (e != cudaSuccess || !split) return e;
+  if (launches) ++*launches;
+  return launch_topk(bh_total * nq, nk, kappa, top_p, logits, kv_index, kv_count, mask, prob, tau, st);
 }
 
 cudaError_t launch_topk(int64_t rows, int64_t nk, int64_t kappa, double top_p, const double *logits,
