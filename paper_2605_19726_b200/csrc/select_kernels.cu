@@ -373,12 +373,18 @@ BA_DEVICE uint32_t lane_id() { return threadIdx.x & 31u; }
 // addition commutes).  A warp holds 8 rows per step, so the per-row work (tree, key store,
 // histogram) costs a quarter of the 16-lane layout's issue slots.
 template <typename T, int D>
-__global__ void __launch_bounds__(256, 3) keys_hist_kernel(SortGeom g, KeysArgs ka, float *__restrict__ keys,
+#ifndef BA_KEYS_RIF
+#define BA_KEYS_RIF 2
+#endif
+#ifndef BA_KEYS_MINB
+#define BA_KEYS_MINB 3
+#endif
+__global__ void __launch_bounds__(256, BA_KEYS_MINB) keys_hist_kernel(SortGeom g, KeysArgs ka, float *__restrict__ keys,
                                                         uint32_t *__restrict__ seg_hist) {
   constexpr int CHUNK = D / 16;                        // features per virtual lane
   constexpr int CB = CHUNK * (int)sizeof(T);           // bytes per chunk: 8, 16 or 32
   constexpr int NV = CB >= 16 ? CB / 16 : 1;           // 16-byte loads per chunk (8-byte chunk: one uint2)
-  constexpr int kRowsInFlight = NV >= 2 ? 1 : 2;       // rows per lane per step (4 chunks each; 128 B in flight)
+  constexpr int kRowsInFlight = NV >= 2 ? 1 : BA_KEYS_RIF;  // rows per lane per step (4 chunks each; 128 B in flight)
   constexpr int kRowsPerStep = 8 * kRowsInFlight;      // per warp
   __shared__ uint32_t hist[2][4][256];  // the chunk's first two segments
   __shared__ int64_t s_seg0;
