@@ -80,6 +80,7 @@ constexpr float kRescaleThreshold = 8.0f;
 #define BA_PP_DEFER_SUM 1
 #endif
 constexpr bool kDeferSum = BA_PP_DEFER_SUM != 0;
+static_assert(kPSplit >= 2, "the first P part is published before the remaining parts (kPSplit 1 is not a layout)");
 constexpr int kMaskWords = 256;                             // nk <= 8192 (L <= 1M tokens)
 constexpr int kTraceTiles = 8;
 constexpr int kDefaultEmu = 1;  // 1 of 8 exp2 pairs on the FMA pipe: +2.4% at A, +1.4% at C (EMU sweep, profiles/round1_microbench.txt)
