@@ -678,10 +678,10 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
   if (emu < 0) {
     const char *e64 = getenv("BA_EXP_EMU");
     emu64 = e64 ? atoi(e64) : kDefaultEmu64;
-    if (emu64 < 0 || emu64 > 2) emu64 = kDefaultEmu64;
+    if (emu64 < 0 || emu64 > 1) emu64 = kDefaultEmu64;
     const char *env = getenv("BA_EXP_EMU");
     emu = env ? atoi(env) : kDefaultEmu;
-    if (emu < 0 || emu > 2) emu = kDefaultEmu;
+    if (emu < 0 || emu > 1) emu = kDefaultEmu;  // 2 of 8 measured slower (profiles/round2_b64_emu.json): not built
     const char *d = getenv("BA_ATTN_DEBUG");
     dbg = d ? atoi(d) : 0;
   }
@@ -695,22 +695,18 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
         return cudaErrorInvalidValue;
       if (a.B == 64) {
         if (e == 0) return launch_variant<128, 0, false, false, true, 3>(a, mk, mv, st);
-        if (e == 2) return launch_variant<128, 2, false, false, true, 3>(a, mk, mv, st);
         return launch_variant<128, 1, false, false, true, 3>(a, mk, mv, st);
       }
       if (e == 1) return launch_variant<128, 1, false, false, false, 3>(a, mk, mv, st);
-      if (e == 2) return launch_variant<128, 2, false, false, false, 3>(a, mk, mv, st);
       return launch_variant<128, 0, false, false, false, 3>(a, mk, mv, st);
     }
     if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, a.B) || !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, a.B))
       return cudaErrorInvalidValue;
     if (a.B == 64) {
       if (e == 0) return launch_variant<128, 0, false, false, true, 1>(a, mk, mv, st);
-      if (e == 2) return launch_variant<128, 2, false, false, true, 1>(a, mk, mv, st);
       return launch_variant<128, 1, false, false, true, 1>(a, mk, mv, st);
     }
     if (e == 1) return launch_variant<128, 1, false, false, false, 1>(a, mk, mv, st);
-    if (e == 2) return launch_variant<128, 2, false, false, false, 1>(a, mk, mv, st);
     return launch_variant<128, 0, false, false, false, 1>(a, mk, mv, st);
   }
   if (!make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, a.B) ||
@@ -728,7 +724,6 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
 #endif
     switch (emu64) {  // exp2 offload for the dual-tile kernel (BA_EXP_EMU; default kDefaultEmu64)
       case 0: return launch_variant<128, 0, false, false, true>(a, mk, mv, st);
-      case 2: return launch_variant<128, 2, false, false, true>(a, mk, mv, st);
       default: return launch_variant<128, 1, false, false, true>(a, mk, mv, st);
     }
   }
@@ -744,7 +739,6 @@ cudaError_t launch_attn_sm100(const AttnArgs &a, cudaStream_t st) {
 #endif
   switch (emu) {
     case 1: return launch_variant<128, 1, false, false>(a, mk, mv, st);
-    case 2: return launch_variant<128, 2, false, false>(a, mk, mv, st);
     default: return launch_variant<128, 0, false, false>(a, mk, mv, st);
   }
 }

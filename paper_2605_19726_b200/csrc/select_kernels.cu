@@ -379,8 +379,8 @@ template <typename T, int D>
 #ifndef BA_KEYS_MINB
 #define BA_KEYS_MINB 3
 #endif
-__global__ void __launch_bounds__(256, BA_KEYS_MINB) keys_hist_kernel(SortGeom g, KeysArgs ka, float *__restrict__ keys,
-                                                        uint32_t *__restrict__ seg_hist) {
+BA_DEVICE void keys_hist_chunk(const SortGeom &g, const KeysArgs &ka, float *__restrict__ keys,
+                                uint32_t *__restrict__ seg_hist, int64_t c) {
   constexpr int CHUNK = D / 16;                        // features per virtual lane
   constexpr int CB = CHUNK * (int)sizeof(T);           // bytes per chunk: 8, 16 or 32
   constexpr int NV = CB >= 16 ? CB / 16 : 1;           // 16-byte loads per chunk (8-byte chunk: one uint2)
@@ -388,8 +388,7 @@ __global__ void __launch_bounds__(256, BA_KEYS_MINB) keys_hist_kernel(SortGeom g
   constexpr int kRowsPerStep = 8 * kRowsInFlight;      // per warp
   __shared__ uint32_t hist[2][4][256];  // the chunk's first two segments
   __shared__ int64_t s_seg0;
-  // CTA -> (side, head row, chunk of kKeysRowsPerCta tokens)
-  int64_t c = blockIdx.x;
+  // chunk c -> (side, head row, chunk of kKeysRowsPerCta tokens)
   const int64_t chunks0 = g.side[0].heads * ((g.side[0].L + kKeysRowsPerCta - 1) / kKeysRowsPerCta);
   const bool s1 = g.n_sides == 2 && c >= chunks0;
   if (s1) c -= chunks0;
@@ -504,6 +503,22 @@ __global__ void __launch_bounds__(256, BA_KEYS_MINB) keys_hist_kernel(SortGeom g
     const uint32_t v = (&hist[sg][0][0])[i & 1023];
     if (v) atomicAdd(&seg_hist[(seg0 + sg) * 1024 + (i & 1023)], v);
   }
+  __syncthreads();  // hist / s_seg0 are reused by the CTA's next chunk
+}
+
+// K1 as one persistent cooperative launch: the CTAs first zero the sort's control block
+// (segment histograms, look-back status, tickets; no stale workspace content survives), one
+// grid-wide barrier, then grid-stride over the 512-row chunks — the memset this replaces
+// was a launch of its own.
+template <typename T, int D>
+__global__ void __launch_bounds__(256, BA_KEYS_MINB) keys_hist_kernel(SortGeom g, KeysArgs ka, float *__restrict__ keys,
+                                                                      uint32_t *__restrict__ seg_hist, uint4 *__restrict__ ctrl,
+                                                                      int64_t ctrl_words, int64_t n_chunks) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ctrl_words; i += (int64_t)gridDim.x * blockDim.x)
+    ctrl[i] = make_uint4(0u, 0u, 0u, 0u);
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) keys_hist_chunk<T, D>(g, ka, keys, seg_hist, c);
 }
 
 BA_DEVICE uint64_t ld_status(const uint64_t *p) {
@@ -660,17 +675,24 @@ cudaError_t launch_keys_sort(const SortGeom &g, int dtype, int d, const KeysArgs
   uint32_t *seg_hist = static_cast<uint32_t *>(ctrl);
   uint64_t *status = reinterpret_cast<uint64_t *>(static_cast<char *>(ctrl) + (size_t)g.segs_total * 1024 * 4);
   uint32_t *tickets = reinterpret_cast<uint32_t *>(status + (size_t)4 * g.tiles_total * 256);
-  cudaError_t e = cudaMemsetAsync(ctrl, 0, sort_ctrl_bytes(g), st);
-  if (e != cudaSuccess) return e;
-  int64_t ctas = 0;
-  for (int s = 0; s < g.n_sides; ++s) ctas += g.side[s].heads * ((g.side[s].L + kKeysRowsPerCta - 1) / kKeysRowsPerCta);
-#define BA_KH(T, D) \
-  keys_hist_kernel<T, D><<<(unsigned)ctas, 256, 0, st>>>(g, ka, reinterpret_cast<float *>(keys_a), seg_hist)
-  if (dtype == 0 && d == 128) BA_KH(__nv_bfloat16, 128);
-  else if (dtype == 0 && d == 64) BA_KH(__nv_bfloat16, 64);
-  else if (dtype == 1 && d == 128) BA_KH(float, 128);
-  else BA_KH(float, 64);
-#undef BA_KH
+  int64_t chunks = 0;
+  for (int s = 0; s < g.n_sides; ++s) chunks += g.side[s].heads * ((g.side[s].L + kKeysRowsPerCta - 1) / kKeysRowsPerCta);
+  void *kernel = dtype == 0 ? (d == 128 ? (void *)keys_hist_kernel<__nv_bfloat16, 128> : (void *)keys_hist_kernel<__nv_bfloat16, 64>)
+                            : (d == 128 ? (void *)keys_hist_kernel<float, 128> : (void *)keys_hist_kernel<float, 64>);
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaError_t e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0)) != cudaSuccess) return e;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+  const unsigned kgrid = (unsigned)std::min<int64_t>(chunks, (int64_t)per_sm * sms);
+  float *keys_f = reinterpret_cast<float *>(keys_a);
+  uint4 *ctrl16 = static_cast<uint4 *>(ctrl);
+  int64_t ctrl_words = (int64_t)((sort_ctrl_bytes(g) + 15) / 16);
+  SortGeom gg = g;
+  KeysArgs kk = ka;
+  void *kargs[] = {&gg, &kk, &keys_f, &seg_hist, &ctrl16, &ctrl_words, &chunks};
+  if ((e = cudaLaunchCooperativeKernel(kernel, dim3(kgrid), dim3(256), kargs, 0, st)) != cudaSuccess) return e;
   uint32_t *kin = keys_a, *vin = vals_a, *kout = keys_b, *vout = vals_b;
   for (int pass = 0; pass < 4; ++pass) {
     const unsigned grid = (unsigned)g.tiles_total;
@@ -683,7 +705,7 @@ cudaError_t launch_keys_sort(const SortGeom &g, int dtype, int d, const KeysArgs
     uint32_t *tk = kin, *tv = vin;
     kin = kout; vin = vout; kout = tk; vout = tv;
   }
-  *launches += 6;  // memset + keys/histograms + 4 passes
+  *launches += 5;  // keys/histograms (zeroing the control block first) + 4 passes
   return cudaGetLastError();
 }
 

@@ -10,4 +10,4 @@ for tool in memcheck racecheck synccheck; do
 done
 timeout 1200 $CS --tool memcheck --target-processes all --print-limit 50 python tools/sanitize_driver.py --tcgen05 > gpurun_out/sanitize_memcheck_tcgen05.txt 2>&1
 echo "rc=$?" >> gpurun_out/sanitize_memcheck_tcgen05.txt
-tail -4 gpurun_out/sanitize_*.txt
+for f in gpurun_out/sanitize_*.txt; do echo "== $f"; tail -3 "$f"; done
