@@ -172,7 +172,7 @@ struct PairWalk {
 template <int kMode, int kEmu, int kGather = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v) {
+               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o) {
   // The whole 227 KB is used, so no room to realign: the dynamic window must
   // start on a 1024-byte boundary (required by the 128-byte swizzle atoms).
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -595,6 +595,10 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     int64_t orow = row0 + r;
     if (r < nrows && a.perm_q) orow = a.perm_q[bh * a.lq + row0 + r];
     const int64_t o_off = b * a.os[0] + h * a.os[1] + orow * a.os[2];
+    // NEXT-2 un-permute by TMA: a full block is staged in this block's (now idle) K/V ring slot
+    // in the 128-byte-swizzled tile layout and written to rows pi_q(i) with tile::scatter4
+    const bool scat = kMode == 0 && a.scatter && nrows == BM;  // warpgroup-uniform
+    const uint32_t stage = base + SMEM_SLOT + (uint32_t)x * TILE;
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
       uint32_t ov[32];
@@ -604,10 +608,36 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
 #pragma unroll
       for (int i = 0; i < 16; ++i)  // l == 0 (empty row): zeros, never unwritten TMEM x 0
         pk[i] = l > 0.f ? pack_bf16(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv) : 0u;
-      if (r < nrows) {
+      if (scat) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // 16-byte chunk cc of row r in box bx (64 columns): swizzled by r & 7
+          const int c = q4 * 4 + i, bx = c >> 3, cc = c & 7;
+          const uint32_t dst = stage + (uint32_t)bx * BOX + (uint32_t)r * 128u + (uint32_t)((cc ^ (r & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(pk[4 * i]), "r"(pk[4 * i + 1]),
+                       "r"(pk[4 * i + 2]), "r"(pk[4 * i + 3])
+                       : "memory");
+        }
+      } else if (r < nrows) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           store_out_row16<__nv_bfloat16>(a, o_off + q4 * 32 + 8 * i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
+      }
+    }
+    if (scat) {
+      fence_proxy_async_smem();  // the generic-proxy smem writes, visible to the TMA unit
+      named_bar_sync(3 + x, 128);
+      if (qd == 0) {  // one warp: lane l scatters rows 4l .. 4l+3 of both 64-column boxes
+        int rr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t tr = row0 + 4 * lane + i;
+          rr[i] = (int)(bh * a.lq + (a.perm_q ? a.perm_q[bh * a.lq + tr] : tr));
+        }
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx)
+          tma_scatter4(stage + (uint32_t)bx * BOX + (uint32_t)lane * 512u, &tm_o, 64 * bx, rr[0], rr[1], rr[2], rr[3]);
+        bulk_commit();
+        bulk_wait_read0();  // shared memory is read before the CTA can exit
       }
     }
     if (a.lse && r < nrows) a.lse[bh * a.lq + orow] = l > 0.f ? (m + log2f(l)) * 0.69314718055994531f : -INFINITY;
@@ -636,8 +666,8 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
 namespace sm100 {
 namespace pp {
 template <int kMode, int kEmu, int kGather = 0>
-cudaError_t launch_mode(const AttnArgs &a, const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, dim3 grid,
-                        cudaStream_t st) {
+cudaError_t launch_mode(const AttnArgs &a, const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv,
+                        const CUtensorMap &mo, dim3 grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel<kMode, kEmu, kGather>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -645,7 +675,7 @@ cudaError_t launch_mode(const AttnArgs &a, const CUtensorMap &mq, const CUtensor
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  attn_pp_kernel<kMode, kEmu, kGather><<<grid, kThreads, SMEM_BYTES, st>>>(a, mq, mk, mv);
+  attn_pp_kernel<kMode, kEmu, kGather><<<grid, kThreads, SMEM_BYTES, st>>>(a, mq, mk, mv, mo);
   return cudaGetLastError();
 }
 }  // namespace pp
@@ -669,9 +699,19 @@ bool attn_pp_supported(const AttnArgs &a) {
 cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
   using namespace sm100;
   using namespace sm100::pp;
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mo;
   if (!get_encode()) return cudaErrorNotSupported;
   const int emu = emu_choice();
+  // NEXT-2 scatter4 epilogue: O dense [b, hq, lq, d] bf16, written to `out` only (no peers / multicast)
+  AttnArgs a2 = a;
+  a2.scatter = 0;
+  static int scat_env = -1;  // BA_PP_SCATTER=0: per-thread row stores (A/B knob)
+  if (scat_env < 0) scat_env = getenv("BA_PP_SCATTER") ? atoi(getenv("BA_PP_SCATTER")) : 1;
+  if (scat_env && a.out && !a.out_mc && a.n_peers == 0 && a.os[2] == a.d && a.os[1] == a.lq * a.d && a.os[0] == a.hq * a.os[1] &&
+      a.lq * a.batch * a.hq < (int64_t)1 << 31 && make_gather_map(&mo, a.out, a.batch, a.hq, a.lq, a.d, a.os))
+    a2.scatter = 1;
+  else
+    mo = mq;  // unused
   dim3 grid((unsigned)((a.nq + 1) / 2), (unsigned)(a.batch * a.hq));
   if (a.gather) {  // bit 1: Q through pi_q (gather4); bit 2: K, V through pi_k (gather4)
     const bool gq = a.gather & 1, gkv = a.gather & 2;
@@ -680,9 +720,9 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
                          : make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) && make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128));
     if (!ok) return cudaErrorInvalidValue;
     // the copy path's exp2-offload variant, so both paths are bit-identical
-    if (gq && gkv) return emu == 0 ? launch_mode<0, 0, 3>(a, mq, mk, mv, grid, st) : launch_mode<0, 1, 3>(a, mq, mk, mv, grid, st);
-    if (gkv) return emu == 0 ? launch_mode<0, 0, 2>(a, mq, mk, mv, grid, st) : launch_mode<0, 1, 2>(a, mq, mk, mv, grid, st);
-    return emu == 0 ? launch_mode<0, 0, 1>(a, mq, mk, mv, grid, st) : launch_mode<0, 1, 1>(a, mq, mk, mv, grid, st);
+    if (gq && gkv) return emu == 0 ? launch_mode<0, 0, 3>(a2, mq, mk, mv, mo, grid, st) : launch_mode<0, 1, 3>(a2, mq, mk, mv, mo, grid, st);
+    if (gkv) return emu == 0 ? launch_mode<0, 0, 2>(a2, mq, mk, mv, mo, grid, st) : launch_mode<0, 1, 2>(a2, mq, mk, mv, mo, grid, st);
+    return emu == 0 ? launch_mode<0, 0, 1>(a2, mq, mk, mv, mo, grid, st) : launch_mode<0, 1, 1>(a2, mq, mk, mv, mo, grid, st);
   }
   if (!make_map(&mq, a.q, a.batch, a.hq, a.lq, a.d, a.qs, 128) || !make_map(&mk, a.k, a.batch, a.hkv, a.lk, a.d, a.ks, 128) ||
       !make_map(&mv, a.v, a.batch, a.hkv, a.lk, a.d, a.vs, 128))
@@ -694,12 +734,12 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
     const char *d = getenv("BA_ATTN_DEBUG");
     dbg = d ? atoi(d) : 0;
   }
-  if (dbg == 1) return launch_mode<1, 0>(a, mq, mk, mv, grid, st);
-  if (dbg == 2) return launch_mode<2, kDefaultEmu>(a, mq, mk, mv, grid, st);
+  if (dbg == 1) return launch_mode<1, 0>(a2, mq, mk, mv, mo, grid, st);
+  if (dbg == 2) return launch_mode<2, kDefaultEmu>(a2, mq, mk, mv, mo, grid, st);
 #endif
   switch (emu) {  // of every 8 exp2 pairs, emu go to the FMA-pipe polynomial
-    case 0: return launch_mode<0, 0>(a, mq, mk, mv, grid, st);
-    default: return launch_mode<0, 1>(a, mq, mk, mv, grid, st);
+    case 0: return launch_mode<0, 0>(a2, mq, mk, mv, mo, grid, st);
+    default: return launch_mode<0, 1>(a2, mq, mk, mv, mo, grid, st);
   }
 }
 

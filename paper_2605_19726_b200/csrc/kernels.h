@@ -142,6 +142,10 @@ struct AttnArgs {
   // One word per error with plain idempotent stores: no read-modify-write, so no
   // system-scope atomics over PCIe are needed.
   unsigned int *err_flag;
+  // set by the pair kernel's launcher (NEXT-2): O is dense [b, hq, lq, d] bf16 and goes to `out`
+  // (no peers / multicast), so full 128-row blocks are staged in shared memory and written to
+  // their rows pi_q(i) by TMA tile::scatter4 (4 rows per instruction) instead of per-thread stores
+  int scatter;
 };
 constexpr int kErrEmptyRow = 0, kErrBadIndex = 1;
 BA_HOST_DEVICE_INLINE void flag_error(unsigned int *f, int which) {

@@ -72,6 +72,18 @@ BA_DEVICE void tma_load_4d(uint32_t dst, const CUtensorMap *m, uint64_t *bar, in
       : "memory");
 }
 
+// TMA tile::scatter4: 4 rows of 64 bf16 columns (512 contiguous bytes of a 128-byte-swizzled
+// tile in shared memory, the layout gather4 loads) to rows r0..r3 at column c0 of a 2-D map.
+BA_DEVICE void tma_scatter4(uint32_t src, const CUtensorMap *m, int c0, int r0, int r1, int r2, int r3) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(src)
+               : "memory");
+}
+BA_DEVICE void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+BA_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+BA_DEVICE void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
 // TMA tile::gather4: rows r0..r3 (row coordinate of a 2-D map), 64 columns from
 // column c0 (the map's box is {64, 1}); the four rows land at dst + 128*i, with
 // the map's 128-byte swizzle applied by smem address like a tile load.

@@ -316,6 +316,37 @@ def test_running_max_grows_every_tile(ba, B):
         assert err.max() <= 1e-3, (h, float(err.max()))
 
 
+def test_pp_scatter4_epilogue_bitwise(ba):
+    """NEXT-2 un-permute by TMA tile::scatter4 (dense O, full 128-row blocks) is bit-identical
+    to per-thread row stores (BA_PP_SCATTER=0), including the ragged last block (always
+    per-thread) and LSE, and both match the oracle."""
+    import os, subprocess, sys
+    code = f"""
+import sys; sys.path.insert(0, {os.path.dirname(__file__)!r}); sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import torch
+import paper_2605_19726_b200.baatt as ba
+from synth import CONFIGS, make_qkv
+w = CONFIGS["C"]
+q, k, v = make_qkv(w, device="cuda", seq_len=128 * 13 + 57, heads_q=4, heads_kv=1, batch=2)
+ctx = ba.Context(q, k, v, 128, 0.5)
+ctx.select(q, k, v)
+out = torch.empty_like(q)
+lse = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+ctx.sparse_attn(out, lse)
+torch.cuda.synchronize()
+torch.save((out.cpu(), lse.cpu()), sys.argv[1])
+print("OK", ba.attention_kernel_name(q, k, v, 128))
+"""
+    outs = []
+    for env_val in ("1", "0"):
+        path = f"/tmp/ba_scatter_{env_val}.pt"
+        env = dict(os.environ, BA_PP_SCATTER=env_val)
+        r = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True, env=env, timeout=240)
+        assert r.returncode == 0 and "OK attn_sm100_tcgen05_pp" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+        outs.append(torch.load(path))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
 def test_pp_unequal_lists_split_steps(ba):
     """Injected lists of unequal lengths (kv_count) with disjoint halves: the pair
     kernel's walk runs shared tiles, split tiles (A and B on different key blocks) and
