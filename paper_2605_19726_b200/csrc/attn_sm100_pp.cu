@@ -80,9 +80,22 @@ constexpr float kRescaleThreshold = 8.0f;
 #define BA_PP_DEFER_SUM 1
 #endif
 constexpr bool kDeferSum = BA_PP_DEFER_SUM != 0;
+#ifndef BA_PP_RELOAD
+#define BA_PP_RELOAD 0
+#endif
+// BA_PP_RELOAD=1: S of P part 1 re-read from TMEM after part 0 is published.  Without it ptxas
+// hoists most of part 1's exps above the first publish (101 of 112 MUFU.EX2 before the first
+// STTM), so both parts go out nearly together; with it the SASS is in program order, but the
+// attention rate is unchanged (A +0.2%, C +-0; profiles/round2_tmem_reload_ab.txt): off.
+constexpr bool kReload = BA_PP_RELOAD != 0;
+static_assert(!kReload || kPSplit == 2, "the reload covers keys 64..127: kPSplit 2");
 static_assert(kPSplit >= 2, "the first P part is published before the remaining parts (kPSplit 1 is not a layout)");
 constexpr int kMaskWords = 256;                             // nk <= 8192 (L <= 1M tokens)
 constexpr int kTraceTiles = 8;
+#ifndef BA_PP_TRACE_START
+#define BA_PP_TRACE_START 32
+#endif
+constexpr int kTraceStart = BA_PP_TRACE_START;  // first traced step (past the pipeline fill)
 constexpr int kDefaultEmu = 1;  // 1 of 8 exp2 pairs on the FMA pipe: +2.4% at A, +1.4% at C (EMU sweep, profiles/round1_microbench.txt)
 constexpr uint32_t SMEM_Q = 0;                              // Q_A, Q_B
 constexpr uint32_t SMEM_SLOT = 2 * TILE;
@@ -187,10 +200,14 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
   // exp2 offload per P part (A/B knobs BA_PP_EMU0 / BA_PP_EMU1; default kEmu for both)
   constexpr int kEmu0 = BA_PP_EMU0 >= 0 ? BA_PP_EMU0 : kEmu, kEmu1 = BA_PP_EMU1 >= 0 ? BA_PP_EMU1 : kEmu;
   constexpr bool kTrace = kMode == 2;
+  // profiling-only skeletons: 1 no softmax; 3 also no K/V/Q loads (full barriers arrived
+  // without a transaction: MMAs on stale shared memory); 4 also no P stores to TMEM
+  constexpr bool kNoSoftmax = kMode == 1 || kMode == 3 || kMode == 4;
+  constexpr bool kNoLoads = kMode == 3 || kMode == 4 || kMode == 5;  // 5: full softmax, no loads (zeroed tiles)
   long long(*trace)[kTraceTiles] = reinterpret_cast<long long(*)[kTraceTiles]>(smem + SMEM_TRACE);
   const bool tr = kTrace && blockIdx.x == 0 && blockIdx.y == 0;
   const long long t_origin = kTrace ? clock64() : 0;
-#define TR(slot, j) do { if (kTrace && tr && (j) < kTraceTiles) trace[slot][j] = clock64() - t_origin; } while (0)
+#define TR(slot, j) do { if (kTrace && tr && (j) >= kTraceStart && (j) < kTraceStart + kTraceTiles) trace[slot][(j) - kTraceStart] = clock64() - t_origin; } while (0)
   const int pair = blockIdx.x;
   const int64_t bh = blockIdx.y;
   const int64_t b = bh / a.hq, h = bh - b * a.hq;
@@ -199,6 +216,8 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
   const int64_t ga = 2 * (int64_t)pair;
   const bool has_b = ga + 1 < a.nq;
 
+  if constexpr (kMode == 5)
+    for (uint32_t i = threadIdx.x; i < SMEM_MASK / 16; i += kThreads) reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0, 0, 0, 0);
   // ---- key-block sets of both query blocks as bitmasks
   for (int w = threadIdx.x; w < 2 * kMaskWords; w += kThreads) mask_a[w] = 0u;
   __syncthreads();
@@ -284,6 +303,8 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
           tma_gather4(dq, &tm_q, &bars.q_full, 0, rr[0], rr[1], rr[2], rr[3]);
           tma_gather4(dq + BOX, &tm_q, &bars.q_full, 64, rr[0], rr[1], rr[2], rr[3]);
         }
+      } else if (kNoLoads && lane == 0) {
+        mbar_arrive(&bars.q_full);
       } else if (lane == 0) {
         mbar_expect_tx(&bars.q_full, 2 * TILE);
         for (int q2 = 0; q2 < 2; ++q2) {  // block B past the end of the sequence is zero-filled
@@ -337,6 +358,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
               const int s = j % kSlots, gk = t ? st.tb : st.ta;
               mbar_wait(&bars.empty[s], ((uint32_t)(j / kSlots) & 1u) ^ 1u);
               if (kv == 0 && t == 0) TR(0, u);
+              if (kNoLoads) { mbar_arrive(&bars.full[s]); continue; }
               const uint32_t dst = base + SMEM_SLOT + s * TILE;
               const CUtensorMap *map = kv ? &tm_v : &tm_k;
               mbar_expect_tx(&bars.full[s], TILE);
@@ -470,9 +492,11 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
     // (S of those columns is already in registers), then p_part[q]
     auto publish_part = [&](int q) {
       constexpr int W = 64 / kPSplit;  // TMEM columns per part
-      if constexpr (W == 32) tmem_st_x32(trow + scol + W * q, pp + W * q);
-      else tmem_st_x16(trow + scol + W * q, pp + W * q);
-      tmem_wait_st();
+      if constexpr (kMode != 4) {
+        if constexpr (W == 32) tmem_st_x32(trow + scol + W * q, pp + W * q);
+        else tmem_st_x16(trow + scol + W * q, pp + W * q);
+        tmem_wait_st();
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.p_part[x][q]);
@@ -483,7 +507,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       mbar_wait(&bars.s_full[x], (uint32_t)u & 1u);
       if (trx) TR(4 + 4 * x, u);
       tc_fence_after();
-      if (kMode == 1) {
+      if (kNoSoftmax) {
 #pragma unroll
         for (int i = 0; i < 64; ++i) pp[i] = 0u;
         if (mine) l = 1.f, m = 0.f;
@@ -557,7 +581,22 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
           exp_pairs(0, PP, f2(-m, -m));
         }
         publish_part(0);
+        if (trx) TR(7 + 4 * x, u);
         const uint64_t nm2 = f2(-m, -m);
+        if constexpr (kReload) {
+          // S of keys 64..127 again from TMEM (P part 0 went to columns 0..31; columns 64..127 are
+          // intact until the next S MMA): the loads are ordered after the tcgen05.st of part 0, so
+          // ptxas cannot hoist the later parts' exps above the first publish (it does otherwise:
+          // 101 of 112 MUFU.EX2 before the first STTM), and PV part 0 overlaps them as intended
+#pragma unroll
+          for (int q4 = 2; q4 < 4; ++q4) tmem_ld_x32(trow + scol + q4 * 32, sr + q4 * 32);
+          tmem_wait_ld();
+          if (u == ragged_step) {
+#pragma unroll
+            for (int i = 64; i < 128; ++i)
+              if (i >= ragged_valid) sr[i] = __float_as_uint(-INFINITY);
+          }
+        }
 #pragma unroll
         for (int h2 = 1; h2 < kPSplit; ++h2) {  // remaining key parts in order; each part's P goes out as soon as done
           exp_pairs(PP * h2, PP * h2 + PP, nm2);
@@ -580,12 +619,11 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
 #pragma unroll
         for (int q = 0; q < kPSplit - 1; ++q) publish_part(q);
       }
-      if (kMode == 1) {
+      if (kNoSoftmax) {
 #pragma unroll
         for (int q = 0; q < kPSplit - 1; ++q) publish_part(q);
       }
-      if (!kDeferSum || kMode == 1 || !mine) publish_part(kPSplit - 1);
-      if (trx) TR(7 + 4 * x, u);
+      if (!kDeferSum || kNoSoftmax || !mine) publish_part(kPSplit - 1);
     }
     if (cnt > 0) {
       mbar_wait(&bars.o_final, 0);
@@ -645,11 +683,11 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
   tc_fence_before();
   __syncthreads();
   if (kTrace && tr && threadIdx.x == 0) {
-    const char *names[12] = {"prod_kv", "mma_pwA", "mma_SA", "mma_pwB", "A_wait", "A_ld", "A_exp", "A_arr",
-                             "B_wait", "B_ld", "B_exp", "B_arr"};
+    const char *names[12] = {"prod_kv", "mma_pwA", "mma_SA", "mma_pwB", "A_wait", "A_ld", "A_end", "A_p0",
+                             "B_wait", "B_ld", "B_end", "B_p0"};
     for (int k2 = 0; k2 < 12; ++k2) {
       printf("TRACE %-8s", names[k2]);
-      for (int j = 0; j < kTraceTiles && j < cnt; ++j) printf(" %7lld", trace[k2][j]);
+      for (int j = 0; j < kTraceTiles && j + kTraceStart < cnt; ++j) printf(" %7lld", trace[k2][j]);
       printf("\n");
     }
   }
@@ -736,6 +774,9 @@ cudaError_t launch_attn_pp(const AttnArgs &a, cudaStream_t st) {
   }
   if (dbg == 1) return launch_mode<1, 0>(a2, mq, mk, mv, mo, grid, st);
   if (dbg == 2) return launch_mode<2, kDefaultEmu>(a2, mq, mk, mv, mo, grid, st);
+  if (dbg == 3) return launch_mode<3, 0>(a2, mq, mk, mv, mo, grid, st);
+  if (dbg == 4) return launch_mode<4, 0>(a2, mq, mk, mv, mo, grid, st);
+  if (dbg == 5) return launch_mode<5, kDefaultEmu>(a2, mq, mk, mv, mo, grid, st);
 #endif
   switch (emu) {  // of every 8 exp2 pairs, emu go to the FMA-pipe polynomial
     case 0: return launch_mode<0, 0>(a2, mq, mk, mv, mo, grid, st);

@@ -8,7 +8,17 @@ using namespace baatt::sm100;
 
 // 0: S TS + PV TS, 1: S SS + PV TS, 2: S SS only, 3: PV TS only,
 // 4: mode 0 + a commit after each 8-MMA group, 5: mode 4 + fence + wait on a completed barrier per group
+// 11: mode 8 without the tcgen05 fence after the K-full wait, 12: mode 8 without any tcgen05 fence after waits
 // 6: the kernel's handoff: S_{j+1} issued, then wait for warp 1 to see S_j complete and arrive, then PV_j
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t r;
+  asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+               : "=r"(r) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return r != 0;
+}
+
+// 13: mode 9 with a CUTLASS-style peek: the K-full barrier of S(j+2) is tested (non-blocking) in the middle of
+//     PV(j)'s MMAs and the blocking wait before S(j+2) is skipped when it was already complete
 template <int MODE>
 __global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) {
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -40,17 +50,20 @@ __global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) 
   const uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | (16u << 17) | (8u << 24);
   const uint32_t IDO = IDS | (1u << 16);
   long long t0 = 0, t1 = 0;
+  constexpr bool P8 = MODE == 8 || MODE == 11 || MODE == 12;  // modes 11-12 are mode 8 variants
+  constexpr bool P9 = MODE == 9 || MODE == 10 || MODE == 13;
+  bool peeked = false;
   if (MODE >= 6) {
     if (threadIdx.x == 0) {
       const uint32_t sk = base + 32768, sv = base + 65536;
       auto issue_s = [&](int j) {
-        if (MODE >= 8 && !(MODE == 10 && j >= 2)) { mbar_wait(&kfull[j & 3], (j >> 2) & 1); tc_fence_after(); }
+        if (MODE >= 8 && !(MODE == 10 && j >= 2) && !(MODE == 13 && peeked)) { mbar_wait(&kfull[j & 3], (j >> 2) & 1); if (MODE < 11) tc_fence_after(); }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
           mma_ts(tmem + (j & 1) * 128, tmem + 384 + kk * 8, make_desc(sk + off, 16, 1024), IDS, kk > 0);
         }
-        if (MODE == 8) mma_commit(&kempty[j & 3]);
+        if (P8) mma_commit(&kempty[j & 3]);
         mma_commit(&sfull[j & 1]);
       };
       t0 = clock64();
@@ -58,23 +71,24 @@ __global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) 
       for (int j = 0; j < iters; ++j) {
         if (j + 1 < iters) issue_s(j + 1);
         mbar_wait(&pfull[j & 1], (j >> 1) & 1);
-        if (MODE == 8) mbar_wait(&vfull[j & 1], (j >> 1) & 1);  // MODE 9: V arrived with K (kfull)
-        tc_fence_after();
+        if (P8) mbar_wait(&vfull[j & 1], (j >> 1) & 1);  // MODE 9: V arrived with K (kfull)
+        if (MODE != 12) tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if (MODE == 10 && kk == 4 && j + 2 < iters) { mbar_wait(&kfull[(j + 2) & 3], ((j + 2) >> 2) & 1); tc_fence_after(); }
+          if (MODE == 13 && kk == 4) peeked = j + 2 < iters && mbar_test(&kfull[(j + 2) & 3], ((j + 2) >> 2) & 1);
           mma_ts(tmem + 256, tmem + (j & 1) * 128 + kk * 8, make_desc(sv + kk * 2048, 16384, 1024), IDO, 1);
         }
-        if (MODE == 8) { mma_commit(&vempty[j & 1]); mma_commit(&odone); }
-        if (MODE >= 9) { mma_commit(&kempty[j & 3]); mma_commit(&odone); }
+        if (P8) { mma_commit(&vempty[j & 1]); mma_commit(&odone); }
+        if (P9) { mma_commit(&kempty[j & 3]); mma_commit(&odone); }
       }
       mma_commit(&bar);
       mbar_wait(&bar, 0);
       t1 = clock64();
       out[blockIdx.x] = t1 - t0;
-    } else if (MODE >= 9 && threadIdx.x == 320) {
+    } else if (P9 && threadIdx.x == 320) {
       for (int j = 0; j < iters; ++j) { mbar_wait(&kempty[j & 3], ((j >> 2) & 1) ^ 1); mbar_arrive(&kfull[j & 3]); }
-    } else if (MODE == 8 && (threadIdx.x == 320 || threadIdx.x == 32)) {
+    } else if (P8 && (threadIdx.x == 320 || threadIdx.x == 32)) {
       // producers without data: wait for the free slot, arrive on the full barrier (K: 4 stages, V: 2)
       const bool is_k = threadIdx.x == 320;
       for (int j = 0; j < iters; ++j) {
@@ -130,9 +144,9 @@ int main() {
   cudaMalloc(&d, 148 * 8);
   const int iters = 2000;
   const char *names[4] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  "};
-  const char *names2[11] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  ", "+commits    ", "+commit+wait", "handoff     ", "handoff x8w ", "+producers  ", "+1 kv ring  ", "kv wait mid "};
-  for (int mode = 0; mode < 11; ++mode) {
-    auto k = mode == 0 ? mma_kernel<0> : mode == 1 ? mma_kernel<1> : mode == 2 ? mma_kernel<2> : mode == 3 ? mma_kernel<3> : mode == 4 ? mma_kernel<4> : mode == 5 ? mma_kernel<5> : mode == 6 ? mma_kernel<6> : mode == 7 ? mma_kernel<7> : mode == 8 ? mma_kernel<8> : mode == 9 ? mma_kernel<9> : mma_kernel<10>;
+  const char *names2[14] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  ", "+commits    ", "+commit+wait", "handoff     ", "handoff x8w ", "+producers  ", "+1 kv ring  ", "kv wait mid ", "8 - kfence  ", "8 - fences  ", "9 + peek    "};
+  for (int mode = 0; mode < 14; ++mode) {
+    auto k = mode == 0 ? mma_kernel<0> : mode == 1 ? mma_kernel<1> : mode == 2 ? mma_kernel<2> : mode == 3 ? mma_kernel<3> : mode == 4 ? mma_kernel<4> : mode == 5 ? mma_kernel<5> : mode == 6 ? mma_kernel<6> : mode == 7 ? mma_kernel<7> : mode == 8 ? mma_kernel<8> : mode == 9 ? mma_kernel<9> : mode == 10 ? mma_kernel<10> : mode == 11 ? mma_kernel<11> : mode == 12 ? mma_kernel<12> : mma_kernel<13>;
 
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     for (int rep = 0; rep < 2; ++rep) {
