@@ -253,7 +253,7 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       bars.n_common = cc;
       bars.n_only_a = ca;
       bars.n_only_b = cb;
-      mbar_init(&bars.q_full, 1);
+      mbar_init(&bars.q_full, (kGather & 1) ? 8 : 1);  // Q through pi_q: one arrive per softmax warp
       for (int s = 0; s < NSLOT; ++s) { mbar_init(&bars.full[s], 1); mbar_init(&bars.empty[s], 1); }
       for (int s = 0; s < 2; ++s) {
         mbar_init(&bars.s_full[s], 1);
@@ -289,20 +289,9 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       const int64_t qb = bh * a.lq;                    // pi_q row base == gather-map row base of (b, h)
       const int64_t kb = (b * a.hkv + hk) * a.lk;      // same for pi_k and the K / V maps
       if constexpr (kGather & 1) {
-        if (lane == 0) mbar_expect_tx(&bars.q_full, 2 * TILE);
-        __syncwarp();
-#pragma unroll
-        for (int q2 = 0; q2 < 2; ++q2) {  // rows past the sequence repeat its last row (never stored)
-          int rr[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int64_t tok = imin64((ga + q2) * BM + 4 * lane + i, a.lq - 1);
-            rr[i] = (int)(qb + __ldg(a.perm_q + qb + tok));
-          }
-          const uint32_t dq = base + SMEM_Q + q2 * TILE + lane * 512;
-          tma_gather4(dq, &tm_q, &bars.q_full, 0, rr[0], rr[1], rr[2], rr[3]);
-          tma_gather4(dq + BOX, &tm_q, &bars.q_full, 64, rr[0], rr[1], rr[2], rr[3]);
-        }
+        // Q through pi_q is loaded by the softmax warps (one row per thread, below): 64
+        // serial tile::gather4 here cost ~4.5k cycles before the first MMA and queued the
+        // first K/V tiles behind them in the TMA unit
       } else if (kNoLoads && lane == 0) {
         mbar_arrive(&bars.q_full);
       } else if (lane == 0) {
@@ -479,6 +468,28 @@ attn_pp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_q, const
       const bool in_a = (mask_a[gl >> 5] >> (gl & 31)) & 1u, in_b = (mask_b[gl >> 5] >> (gl & 31)) & 1u;
       if (in_a && in_b) ragged_step = n_common - 1;
       else if (x ? in_b : in_a) ragged_step = n_mine - 1;
+    }
+    if constexpr ((kGather & 1) != 0) {
+      if (cnt > 0) {
+        // NEXT-2 Q in place: row r of query block x is row pi_q(row0 + r) of the original Q (rows past
+        // the sequence repeat its last row; they are never stored), 16 independent 16-byte loads
+        // written into the 128-byte-swizzled K-major tile the S MMA reads
+        const int64_t tok = imin64(row0 + r, a.lq - 1);
+        const int64_t src_row = __ldg(a.perm_q + bh * a.lq + tok);
+        const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(a.q) + b * a.qs[0] +
+                                                           h * a.qs[1] + src_row * a.qs[2]);
+        uint4 qv[16];
+#pragma unroll
+        for (int c16 = 0; c16 < 16; ++c16) qv[c16] = __ldg(src + c16);
+#pragma unroll
+        for (int c16 = 0; c16 < 16; ++c16) {
+          const int bx = c16 >> 3, cc = c16 & 7;
+          *reinterpret_cast<uint4 *>(smem + SMEM_Q + x * TILE + bx * BOX + r * 128 + ((cc ^ (r & 7)) << 4)) = qv[c16];
+        }
+        fence_proxy_async_smem();  // generic-proxy smem writes, visible to the tensor core's reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.q_full);
+      }
     }
     const float c = a.scale * 1.4426950408889634f;
     float m = -INFINITY, l = 0.f;
