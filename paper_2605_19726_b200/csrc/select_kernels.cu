@@ -1523,12 +1523,46 @@ BA_DEVICE void topk_row(int64_t row, int64_t nk, int64_t kappa, double top_p, co
     }
     const unsigned ball = __ballot_sync(0xffffffffu, dsel >= 0);
     const int owner = __ffs(ball) - 1;
+    const unsigned c_bin = hist[dsel < 0 ? 0 : dsel];  // read before the shuffle (owner's dsel is valid)
     dsel = __shfl_sync(0xffffffffu, dsel, owner);
     before = __shfl_sync(0xffffffffu, before, owner);
+    const unsigned n_bin = __shfl_sync(0xffffffffu, c_bin, owner);  // candidates sharing the new prefix
     k_rem -= before;
     T |= (uint64_t)dsel << shift;
     pmask |= 0xFFull << shift;
     __syncwarp();
+    if (pass < 7 && n_bin <= 32) {
+      // at most 32 candidates left: one per lane, and the k_rem-th largest of them is T, found by
+      // counting, for each, the candidates above it (the same T and tie count the remaining radix
+      // passes would reach)
+      uint64_t *cs = reinterpret_cast<uint64_t *>(hist);  // this pass's histogram is consumed: 128 slots
+      unsigned base_n = 0;
+      for (int64_t j0 = 0; j0 < nk && base_n < n_bin; j0 += 32) {  // warp-uniform bound
+        const int64_t j = j0 + lane;
+        const uint64_t v = j < nk ? u[j] : 0ull;
+        const bool in = j < nk && (v & pmask) == T;
+        const unsigned m = __ballot_sync(0xffffffffu, in);
+        if (in) cs[base_n + __popc(m & lanemask_lt())] = v;
+        base_n += __popc(m);
+      }
+      __syncwarp();
+      const bool have = (unsigned)lane < n_bin;
+      const uint64_t cand = have ? cs[lane] : 0ull;
+      __syncwarp();
+      unsigned gt = 0, ge = 0;
+#pragma unroll 1
+      for (int i = 0; i < (int)n_bin; ++i) {
+        const uint64_t o = __shfl_sync(0xffffffffu, cand, i);
+        gt += o > cand;
+        ge += o >= cand;
+      }
+      const bool is_t = have && gt < k_rem && k_rem <= ge;
+      const unsigned tb = __ballot_sync(0xffffffffu, is_t);
+      const int tl = __ffs(tb) - 1;
+      T = __shfl_sync(0xffffffffu, cand, tl);
+      k_rem -= __shfl_sync(0xffffffffu, gt, tl);
+      break;
+    }
   }
   const unsigned need_eq = k_rem;  // equal-to-T entries still needed (>= 1); the rest are > T
   unsigned eq_seen = 0, sel_seen = 0;
