@@ -17,6 +17,10 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
   return r != 0;
 }
 
+// 15: mode 9 without the MMA thread's K-full wait (producer and commits unchanged; data race irrelevant here)
+// 17: mode 7 + one extra commit (kempty) after PV; 18: mode 16 with the two commits issued before PV instead of after
+// 16: mode 7 + the kempty / odone commits of mode 9 (no producer, no K-full wait)
+// 14: mode 9 with the producer polling its empty barrier by test_wait + nanosleep(128) instead of try_wait
 // 13: mode 9 with a CUTLASS-style peek: the K-full barrier of S(j+2) is tested (non-blocking) in the middle of
 //     PV(j)'s MMAs and the blocking wait before S(j+2) is skipped when it was already complete
 template <int MODE>
@@ -51,13 +55,13 @@ __global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) 
   const uint32_t IDO = IDS | (1u << 16);
   long long t0 = 0, t1 = 0;
   constexpr bool P8 = MODE == 8 || MODE == 11 || MODE == 12;  // modes 11-12 are mode 8 variants
-  constexpr bool P9 = MODE == 9 || MODE == 10 || MODE == 13;
+  constexpr bool P9 = MODE == 9 || MODE == 10 || MODE == 13 || MODE == 14 || MODE == 15;
   bool peeked = false;
   if (MODE >= 6) {
     if (threadIdx.x == 0) {
       const uint32_t sk = base + 32768, sv = base + 65536;
       auto issue_s = [&](int j) {
-        if (MODE >= 8 && !(MODE == 10 && j >= 2) && !(MODE == 13 && peeked)) { mbar_wait(&kfull[j & 3], (j >> 2) & 1); if (MODE < 11) tc_fence_after(); }
+        if (MODE >= 8 && MODE != 15 && MODE < 16 && !(MODE == 10 && j >= 2) && !(MODE == 13 && peeked)) { mbar_wait(&kfull[j & 3], (j >> 2) & 1); if (MODE < 11) tc_fence_after(); }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -73,6 +77,7 @@ __global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) 
         mbar_wait(&pfull[j & 1], (j >> 1) & 1);
         if (P8) mbar_wait(&vfull[j & 1], (j >> 1) & 1);  // MODE 9: V arrived with K (kfull)
         if (MODE != 12) tc_fence_after();
+        if (MODE == 18) { mma_commit(&kempty[j & 3]); mma_commit(&odone); }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if (MODE == 10 && kk == 4 && j + 2 < iters) { mbar_wait(&kfull[(j + 2) & 3], ((j + 2) >> 2) & 1); tc_fence_after(); }
@@ -80,14 +85,19 @@ __global__ void __launch_bounds__(352, 1) mma_kernel(int iters, long long *out) 
           mma_ts(tmem + 256, tmem + (j & 1) * 128 + kk * 8, make_desc(sv + kk * 2048, 16384, 1024), IDO, 1);
         }
         if (P8) { mma_commit(&vempty[j & 1]); mma_commit(&odone); }
-        if (P9) { mma_commit(&kempty[j & 3]); mma_commit(&odone); }
+        if (P9 || MODE == 16) { mma_commit(&kempty[j & 3]); mma_commit(&odone); }
+        if (MODE == 17) mma_commit(&kempty[j & 3]);
       }
       mma_commit(&bar);
       mbar_wait(&bar, 0);
       t1 = clock64();
       out[blockIdx.x] = t1 - t0;
     } else if (P9 && threadIdx.x == 320) {
-      for (int j = 0; j < iters; ++j) { mbar_wait(&kempty[j & 3], ((j >> 2) & 1) ^ 1); mbar_arrive(&kfull[j & 3]); }
+      for (int j = 0; j < iters; ++j) {
+        if (MODE == 14) { while (!mbar_test(&kempty[j & 3], ((j >> 2) & 1) ^ 1)) __nanosleep(128); }
+        else mbar_wait(&kempty[j & 3], ((j >> 2) & 1) ^ 1);
+        mbar_arrive(&kfull[j & 3]);
+      }
     } else if (P8 && (threadIdx.x == 320 || threadIdx.x == 32)) {
       // producers without data: wait for the free slot, arrive on the full barrier (K: 4 stages, V: 2)
       const bool is_k = threadIdx.x == 320;
@@ -144,9 +154,9 @@ int main() {
   cudaMalloc(&d, 148 * 8);
   const int iters = 2000;
   const char *names[4] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  "};
-  const char *names2[14] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  ", "+commits    ", "+commit+wait", "handoff     ", "handoff x8w ", "+producers  ", "+1 kv ring  ", "kv wait mid ", "8 - kfence  ", "8 - fences  ", "9 + peek    "};
-  for (int mode = 0; mode < 14; ++mode) {
-    auto k = mode == 0 ? mma_kernel<0> : mode == 1 ? mma_kernel<1> : mode == 2 ? mma_kernel<2> : mode == 3 ? mma_kernel<3> : mode == 4 ? mma_kernel<4> : mode == 5 ? mma_kernel<5> : mode == 6 ? mma_kernel<6> : mode == 7 ? mma_kernel<7> : mode == 8 ? mma_kernel<8> : mode == 9 ? mma_kernel<9> : mode == 10 ? mma_kernel<10> : mode == 11 ? mma_kernel<11> : mode == 12 ? mma_kernel<12> : mma_kernel<13>;
+  const char *names2[19] = {"S TS + PV TS", "S SS + PV TS", "S SS only   ", "PV TS only  ", "+commits    ", "+commit+wait", "handoff     ", "handoff x8w ", "+producers  ", "+1 kv ring  ", "kv wait mid ", "8 - kfence  ", "8 - fences  ", "9 + peek    ", "9 + sleepy p", "9 - kwait   ", "7 + commits ", "7 + 1 commit", "7 + 2c early"};
+  for (int mode = 0; mode < 19; ++mode) {
+    auto k = mode == 0 ? mma_kernel<0> : mode == 1 ? mma_kernel<1> : mode == 2 ? mma_kernel<2> : mode == 3 ? mma_kernel<3> : mode == 4 ? mma_kernel<4> : mode == 5 ? mma_kernel<5> : mode == 6 ? mma_kernel<6> : mode == 7 ? mma_kernel<7> : mode == 8 ? mma_kernel<8> : mode == 9 ? mma_kernel<9> : mode == 10 ? mma_kernel<10> : mode == 11 ? mma_kernel<11> : mode == 12 ? mma_kernel<12> : mode == 13 ? mma_kernel<13> : mode == 14 ? mma_kernel<14> : mode == 15 ? mma_kernel<15> : mode == 16 ? mma_kernel<16> : mode == 17 ? mma_kernel<17> : mma_kernel<18>;
 
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     for (int rep = 0; rep < 2; ++rep) {
