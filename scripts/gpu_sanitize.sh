@@ -1,4 +1,5 @@
 #!/bin/bash
+# (compute-sanitizer has since been closed on the GPU pool: the runs kept in profiles/ are from round 2, e541b0c)
 # compute-sanitizer memcheck / racecheck / synccheck on the selection kernels (K1-K4) and the
 # SIMT attention (K6) over small ragged problems (tools/sanitize_driver.py); summaries -> gpurun_out/
 set -u

@@ -25,6 +25,11 @@ for cfg, L, hq, hkv, B, kw in (("T", 1024 + 37, 1, 1, 64, {}),
     if q.dtype == torch.float32 or tc:
         out = torch.empty_like(q)
         ctx.sparse_attn(out)
+    if tc and q.dtype == torch.bfloat16 and ba.q_gather_supported(q, k, v, B):
+        # NEXT-2 Q in place: the pair kernel's softmax warps load Q rows through pi_q
+        zq = ba.Context(q, k, v, B, 0.5, zero_copy="q")
+        zq.select(q, k, v)
+        zq.sparse_attn(torch.empty_like(q))
     torch.cuda.synchronize()
     print(cfg, L, "ok", flush=True)
 print("done")
