@@ -64,6 +64,36 @@ def test_selection_bf16(ba, cfg, L, hq, hkv, dens, comp):
     assert rep["max_stat_err"] < 1e-12, rep
 
 
+@pytest.mark.parametrize("B,nk,n_tie", [(128, 24, 12), (128, 64, 20), (64, 96, 30)])
+def test_topk_exact_ties_take_lower_blocks(ba, B, nk, n_tie):
+    """Score ties -> lower g_k (reading A3) with EXACT logit ties: sort='none' keeps the
+    blocks contiguous, so n_tie copies of one K block have bit-identical block stats and logits
+    on both sides.  The tie group straddles the kappa-th largest in most rows, which runs the
+    top-kappa's <= 32-candidate finish (nk 24: from the first radix pass; nk 64 / 96: after the
+    passes that isolate the group).  Checked: P4 against the oracle, exact ties in the GPU's
+    logits, and in every row the selected members of the group are its lowest-index ones."""
+    w = CONFIGS["A"]
+    q, k, v = make_qkv(w, device="cuda", seq_len=nk * B, heads_q=2, heads_kv=1)
+    rng = np.random.default_rng(nk)
+    tie = np.sort(rng.choice(nk, n_tie, replace=False))
+    for g in tie[1:]:
+        k[:, :, g * B:(g + 1) * B] = k[:, :, tie[0] * B:(tie[0] + 1) * B]
+    _, sel = _run_select(ba, q, k, v, B, 0.5, sort="none")
+    check_selection(sel, oracle_select_all(q, k, B, 0.5, 1.0, "none", "diag"))
+    lg = sel.logits.cpu().numpy()
+    assert (lg[..., tie] == lg[..., tie[:1]]).all(), "copies of one key block must tie exactly"
+    mask = sel.mask.cpu().numpy().astype(bool)
+    partial = 0
+    for b_ in range(mask.shape[0]):
+        for h in range(mask.shape[1]):
+            for g in range(mask.shape[2]):
+                chosen = mask[b_, h, g, tie]
+                n = int(chosen.sum())
+                assert chosen[:n].all() and not chosen[n:].any(), (h, g, chosen)
+                partial += 0 < n < n_tie
+    assert partial > 0, "no row split the tie group: the case under test did not occur"
+
+
 @pytest.mark.parametrize("cfg,L,hq,hkv,B", [("A", 4096 + 77, 4, 4, 128), ("C", 8192, 8, 2, 128), ("T", 1024, 1, 1, 64),
                                           ("M", 4096 + 17, 2, 2, 64)])
 def test_norm_order_against_exact_norms(ba, cfg, L, hq, hkv, B):
