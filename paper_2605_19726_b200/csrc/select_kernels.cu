@@ -1205,7 +1205,7 @@ BA_DEVICE void scores_tile(int64_t hq, int64_t grp, int64_t nq, int64_t nk, cons
 // the operand arrays that stage's feature part needs (a stage never straddles a part).
 // Measured (ncu, config A) the 32 x 32 form stalled on smem fragment latency (short
 // scoreboard 19%) and barriers (14%) as much as on the FP64 pipe (20%).
-constexpr int kScW_KS = 16, kScW_LDS = 128 + 8;
+constexpr int kScW_KS = 16, kScW_LDS = 128 + 4;  // +4: the 4 fragment rows tq of a half-warp fall on distinct bank groups
 struct ScoresSmemW {
   double A[2][kScW_KS][kScW_LDS];
   double B[2][kScW_KS][kScW_LDS];
