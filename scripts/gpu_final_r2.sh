@@ -15,7 +15,7 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref
 for f in C A M V C_random ref; do python -c "import json,sys; d=json.load(open('$O/bench_$f.json')); r=d.get('roofline') or {}; print('$f', round(d['value'],3), d['unit'], 'attn', r.get('achieved'), 'frac', r.get('frac'), 'sel_share', d.get('select_share'), 'dense', d.get('dense_tflops'), 'sdpa', d.get('sdpa_tflops'), 'e2e', (d.get('e2e') or {}).get('value'), 'mhz', (d.get('clocks') or {}).get('sm_mhz'), (d.get('clocks') or {}).get('reasons'))" 2>&1 | tail -1; done
 args=()
 for c in C A M; do
-  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  timeout 1400 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $O/launches_$c.csv python bench.py --config $c --profile --no-e2e --no-cpu --no-dense --steps 2 --warmup 1 > $O/launches_$c.log 2>&1
   python tools/launches.py $O/launches_$c.csv > $O/launches_$c.txt 2>&1
   kn=$(tail -1 $O/launches_$c.log | python -c "import json,sys; print(json.loads(sys.stdin.read())['roofline']['kernel'])")
