@@ -11,5 +11,5 @@ for r in 1 2; do for c in A C M; do for v in new old; do
 done; done; done
 for v in new old; do
   L=paper_2605_19726_b200/libbaatt.so; [ $v = old ] && L=paper_2605_19726_b200/libbaatt_old.so
-  BA_LIB_PATH=$L timeout 600 ncu --metrics gpu__time_duration.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum --clock-control none -k regex:"scores_topk|onesweep" --csv python bench.py --config M --profile --no-e2e --no-cpu --no-dense --steps 1 --warmup 0 2>/dev/null | grep -E "duration" | awk -F'","' -v v=$v '{print v, $(NF-2), $NF}'
+  BA_LIB_PATH=$L timeout 600 ncu --metrics gpu__time_duration.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum --clock-control none -k regex:"topk_kernel" --csv python bench.py --config M --profile --no-e2e --no-cpu --no-dense --steps 1 --warmup 0 2>/dev/null | grep -E "duration" | awk -F'","' -v v=$v '{print v, $(NF-2), $NF}'
 done
